@@ -1,0 +1,325 @@
+"""Pins of the FP64 oracle against what the paper and mathematics fix.
+
+None of these re-types the oracle's own formula: each check is a closed form, an
+independent library routine (numpy QR/cholesky/lstsq, scikit-learn), brute force,
+an invariant, or a hand-derived worked example stored under tests/golden/.
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import DEGENERATE, EPS, MAXITER, NAN, omp, omp_batch
+from oracle.exhaustive import exhaustive_best_support
+from oracle.inv_chol import chol_append, inv_chol_append, ls_by_inverse_cholesky
+from oracle.omp_oracle import least_squares_residual
+from synth import make_dictionary, make_problem, make_signals
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
+
+
+def _gauss(M, N, seed, normalize=True):
+    A = np.random.default_rng(seed).standard_normal((M, N))
+    if normalize:
+        A /= np.linalg.norm(A, axis=0)
+    return A
+
+
+def _residual(A, y, res):
+    return np.asarray(y, float) - np.asarray(A, float)[:, res.support] @ res.x
+
+
+# ---------------------------------------------------------------- P5: worked examples
+@pytest.mark.parametrize("ex", GOLD["omp"], ids=[e["name"] for e in GOLD["omp"]])
+def test_p5_worked_examples(ex):
+    A = np.array(ex["A_columns"], dtype=float).T
+    y = np.array(ex["y"])
+    res = omp(A, y, ex["S"], ex.get("eps"))
+    e = ex["expect"]
+    assert res.status == STATUS[e["status"]]
+    assert list(res.support) == e["support"]
+    np.testing.assert_allclose(res.x, e["x"], atol=1e-12)
+    np.testing.assert_allclose([s.resid_norm for s in res.steps], e["resid_norms"], atol=1e-12)
+    if "correlations_step1" in e:
+        np.testing.assert_allclose(A.T @ y, e["correlations_step1"], atol=1e-12)
+        r1 = y - A[:, e["support"][:1]] @ np.array([A[:, e["support"][0]] @ y])
+        np.testing.assert_allclose(A.T @ r1, e["correlations_step2"], atol=1e-12)
+
+
+def test_p5_inverse_cholesky_worked_example():
+    ex = GOLD["factor"][0]
+    A = np.array(ex["A_columns"], dtype=float).T
+    e = ex["expect"]
+    F1, _, g1 = inv_chol_append(None, np.zeros(0), 1.0)
+    np.testing.assert_allclose(F1, e["F1"], atol=0)
+    F2, z2, g2 = inv_chol_append(F1, np.array(e["w2"]), e["d2"])
+    np.testing.assert_allclose(z2, e["z2"], atol=1e-15)
+    assert g2 == pytest.approx(e["gamma2"], abs=1e-14)
+    np.testing.assert_allclose(F2, e["F2"], atol=1e-14)
+    V2 = chol_append(chol_append(None, np.zeros(0), 1.0), np.array(e["w2"]), e["d2"])
+    np.testing.assert_allclose(V2, e["V2"], atol=1e-15)
+    np.testing.assert_allclose(F2 @ V2.T, np.eye(2), atol=1e-15)
+    x, Fs, _ = ls_by_inverse_cholesky(A, ex["y"], ex["support"])
+    np.testing.assert_allclose(x, e["x2"], atol=1e-14)
+    u = F2.T @ (A.T @ np.array(ex["y"]))
+    np.testing.assert_allclose(u, e["u2"], atol=1e-14)
+
+
+def test_p5_cholesky_and_forward_solve_examples():
+    c = GOLD["cholesky"]
+    np.testing.assert_allclose(np.linalg.cholesky(np.array(c["gram"])), c["V"], atol=1e-15)
+    V = chol_append(chol_append(None, np.zeros(0), 1.0), np.array([0.6]), 1.0)
+    np.testing.assert_allclose(V, c["V"], atol=1e-15)
+    # forward substitution inside chol_append: V_{k-1} z = w with V = [[2,0],[1,1]], w=(2,3)
+    Vf = np.array(c["forward_V"])
+    V3 = chol_append(Vf, np.array(c["forward_rhs"]), 100.0)
+    np.testing.assert_allclose(V3[2, :2], c["forward_z"], atol=1e-15)
+
+
+def test_p5_argmax_examples():
+    g = GOLD["argmax"]
+    # selection of the oracle on A = I with r = each row (|<r,e_n>| = |r_n|)
+    for row, want in zip(g["rows"], g["argmax"]):
+        r = np.array(row)
+        if not np.any(r):
+            # exhausted residual: the oracle stops DEGENERATE (reading R6) after reporting n* = 0
+            res = omp(np.eye(3), r, 1)
+            assert res.status == DEGENERATE and res.steps[0].n_star == want
+        else:
+            res = omp(np.eye(3), r, 1)
+            assert res.support[0] == want
+
+
+# ---------------------------------------------------------------- P1: orthonormal closed form
+@pytest.mark.parametrize("kind", ["random_orthogonal", "identity"])
+def test_p1_orthonormal_closed_form(kind):
+    rng = np.random.default_rng(11)
+    n = 64
+    Q = np.linalg.qr(rng.standard_normal((n, n)))[0] if kind != "identity" else np.eye(n)
+    y = rng.standard_normal(n)
+    if kind == "identity":
+        y[[5, 9]] = 4.0   # exact tie in |A^T y| -> lowest index first
+        y[17] = -4.0
+    S = 12
+    c = Q.T @ y
+    order = np.argsort(-np.abs(c), kind="stable")[:S]   # k-th largest |a^T y|, lowest index on ties
+    res = omp(Q, y, S)
+    assert list(res.support) == list(order)
+    np.testing.assert_allclose(res.x, c[order], atol=1e-12)
+    want_r2 = y @ y - np.cumsum(c[order] ** 2)
+    got_r2 = np.array([s.resid_norm for s in res.steps]) ** 2
+    np.testing.assert_allclose(got_r2, want_r2, atol=1e-12)
+
+
+# ---------------------------------------------------------------- P2: orthogonality + monotonicity
+@pytest.mark.parametrize("sigma", [0.0, 0.05])
+def test_p2_residual_orthogonal_and_monotone(sigma):
+    A = _gauss(32, 64, 3, normalize=False)   # raw norms: selection must divide by ||a_n||
+    rng = np.random.default_rng(4)
+    for trial in range(5):
+        x = np.zeros(64)
+        x[rng.choice(64, 6, replace=False)] = rng.standard_normal(6)
+        y = A @ x + sigma * rng.standard_normal(32)
+        S = 12
+        full = omp(A, y, S)
+        norms = [s.resid_norm for s in full.steps if np.isfinite(s.resid_norm)]
+        assert len(norms) == full.n_iter
+        assert all(b <= a + 1e-12 * np.linalg.norm(y) for a, b in zip(norms, norms[1:]))
+        for k in range(1, full.n_iter + 1):
+            pre = omp(A, y, k)                      # Alg. 1 is a prefix process
+            assert list(pre.support) == list(full.support[:k])
+            r = _residual(A, y, pre)
+            a = A[:, pre.support]
+            assert np.max(np.abs(a.T @ r) / np.linalg.norm(a, axis=0)) <= 1e-12 * np.linalg.norm(y)
+
+
+# ---------------------------------------------------------------- P3: exact recovery
+def test_p3_exact_recovery_tiny_fixed_seed():
+    prob = make_problem("tiny", with_truth=True)
+    out = omp_batch(prob.A, prob.Y, prob.S, workers=1)
+    for res, supp, coef in zip(out, prob.truth.supports, prob.truth.coefs):
+        assert set(res.support) == set(supp)
+        got = res.dense(prob.N)[supp]
+        np.testing.assert_allclose(got, coef, rtol=0, atol=1e-5 * np.linalg.norm(coef))
+        assert res.resid_norm <= 1e-6 * res.y_norm
+
+
+def test_p3_exact_recovery_rate_tiny_and_c2():
+    prob = make_problem("tiny", B=400, with_truth=True)
+    out = omp_batch(prob.A, prob.Y, prob.S, workers=4)
+    ok = np.mean([set(r.support) == set(s) for r, s in zip(out, prob.truth.supports)])
+    assert ok >= 0.99
+    prob = make_problem("c2", B=8, with_truth=True)
+    out = omp_batch(prob.A, prob.Y, prob.S, workers=4)
+    assert all(set(r.support) == set(s) for r, s in zip(out, prob.truth.supports))
+
+
+# ---------------------------------------------------------------- P4: brute force
+def test_p4_brute_force_subsets_and_prefixes_tiny():
+    prob = make_problem("tiny")
+    for y in prob.Y[:16]:
+        res = omp(prob.A, y, prob.S)
+        supp = list(res.support)
+        full = least_squares_residual(prob.A, y, supp)
+        assert full == pytest.approx(res.resid_norm, abs=1e-12)
+        for mask in range(1 << len(supp)):
+            T = [s for i, s in enumerate(supp) if mask >> i & 1]
+            rT = least_squares_residual(prob.A, y, T)
+            if len(T) < len(supp):
+                assert rT >= full - 1e-12
+        A64 = prob.A.astype(float)
+        for k in range(1, len(supp) + 1):
+            pre = omp(prob.A, y, k)
+            xt, *_ = np.linalg.lstsq(A64[:, supp[:k]], y.astype(float), rcond=None)
+            np.testing.assert_allclose(pre.x, xt, atol=1e-12 * max(1.0, np.abs(xt).max()))
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.05])
+def test_p4_exhaustive_global_optimum_tiny(sigma):
+    A = make_dictionary(32, 64, 1)
+    Y = make_signals(A, range(4), 1, 4, sigma)
+    for y in Y:
+        res = omp(A, y, 4)
+        best, best_r = exhaustive_best_support(A, y, 4)
+        assert res.resid_norm >= best_r - 1e-12       # greedy never beats the global optimum
+        if sigma == 0.0:
+            assert set(best) == set(res.support)      # [measured in SURVEY: 16/16 at sigma = 0]
+
+
+def test_p4_greedy_vs_exhaustive_small_instances():
+    rng = np.random.default_rng(7)
+    strict = 0
+    for i in range(100):
+        A = rng.standard_normal((6, 10))
+        A /= np.linalg.norm(A, axis=0)
+        if i % 2 == 0:
+            x = np.zeros(10)
+            x[rng.choice(10, 2, replace=False)] = rng.standard_normal(2)
+            y = A @ x
+        else:
+            y = rng.standard_normal(6)
+        res = omp(A, y, 2)
+        best, best_r = exhaustive_best_support(A, y, 2)
+        assert res.resid_norm >= best_r - 1e-12
+        if i % 2 == 0:
+            assert best_r <= 1e-10
+        strict += res.resid_norm > best_r + 1e-9
+    assert strict >= 1   # "does not necessarily converge to the global optimum"
+
+
+# ---------------------------------------------------------------- P6: library routine
+def test_p6_matches_sklearn_orthogonal_mp():
+    from sklearn.linear_model import orthogonal_mp
+    A = _gauss(32, 64, 21)
+    rng = np.random.default_rng(22)
+    Y = np.stack([A[:, rng.choice(64, 4, replace=False)] @ rng.standard_normal(4)
+                  + 0.05 * rng.standard_normal(32) for _ in range(16)])
+    coef = orthogonal_mp(A, Y.T, n_nonzero_coefs=6)
+    for b in range(16):
+        res = omp(A, Y[b], 6)
+        np.testing.assert_allclose(res.dense(64), coef[:, b], atol=1e-10)
+
+
+# ---------------------------------------------------------------- P7: normalisation invariance
+def test_p7_column_scaling_invariance():
+    A = _gauss(32, 64, 31)
+    rng = np.random.default_rng(32)
+    D = rng.uniform(0.25, 4.0, 64)
+    for _ in range(5):
+        y = A[:, rng.choice(64, 5, replace=False)] @ rng.standard_normal(5) + 0.01 * rng.standard_normal(32)
+        r1 = omp(A, y, 8)
+        r2 = omp(A * D, y, 8)
+        assert list(r1.support) == list(r2.support)
+        np.testing.assert_allclose(r2.x, r1.x / D[r1.support], rtol=1e-10)   # App. A
+
+
+# ---------------------------------------------------------------- P8: batch invariance
+def test_p8_batch_and_worker_invariance():
+    p10 = make_problem("c2", B=10)
+    p1 = make_problem("c2", indices=[7])
+    assert np.array_equal(p10.Y[7], p1.Y[0])
+    serial = omp_batch(p10.A, p10.Y, 8, workers=1)
+    par = omp_batch(p10.A, p10.Y, 8, workers=3, chunk=2)
+    for a, b in zip(serial, par):
+        assert list(a.support) == list(b.support) and np.array_equal(a.x, b.x)
+
+
+# ---------------------------------------------------------------- P9: inverse-Cholesky identities
+def test_p9_inverse_cholesky_identities():
+    prob = make_problem("c2", B=3)
+    A64 = prob.A.astype(float)
+    for y32 in prob.Y:
+        y = y32.astype(float)
+        res = omp(prob.A, y32, 16)
+        supp = list(res.support)
+        x, Fs, gammas = ls_by_inverse_cholesky(prob.A, y, supp)
+        np.testing.assert_allclose(x, res.x, rtol=1e-10, atol=1e-12)
+        for k in range(1, len(supp) + 1):
+            A_k = A64[:, supp[:k]]
+            V = np.linalg.cholesky(A_k.T @ A_k)                 # independent library factor
+            np.testing.assert_allclose(Fs[k - 1] @ V.T, np.eye(k), atol=1e-12)
+            u = Fs[k - 1].T @ (A_k.T @ y)
+            r_k = y - A_k @ (Fs[k - 1] @ u)
+            assert r_k @ r_k == pytest.approx(y @ y - u @ u, abs=1e-11 * (y @ y))   # Pythagoras
+            r_prev = y - A64[:, supp[:k - 1]] @ omp(prob.A, y32, k - 1).x if k > 1 else y
+            c_star = A64[:, supp[k - 1]] @ r_prev
+            assert u[-1] == pytest.approx(gammas[k - 1] * c_star, abs=1e-11 * np.linalg.norm(y))
+
+
+# ---------------------------------------------------------------- P10: eps and degenerate edges
+def test_p10_eps_edges():
+    prob = make_problem("c2", B=2)
+    y = prob.Y[0]
+    yn = float(np.linalg.norm(y.astype(float)))
+    r = omp(prob.A, y, 8, eps=yn * 1.5)
+    assert r.status == EPS and r.n_iter == 0 and r.x.size == 0
+    r = omp(prob.A, y, 8, eps=1e-9)
+    assert r.status == MAXITER and r.n_iter == 8 and r.resid_norm > 1e-9
+    r = omp(prob.A, y, 8, eps=None)
+    assert r.status == MAXITER
+    r = omp(prob.A, y, 8, eps=-1.0)         # negative eps means "no tolerance"
+    assert r.status == MAXITER
+    full = omp(prob.A, y, 32)
+    target = full.steps[9].resid_norm
+    r = omp(prob.A, y, 32, eps=target * (1 + 1e-3))
+    assert r.status == EPS and r.n_iter == 10 and r.resid_norm <= target * (1 + 1e-3)
+    assert r.steps[-2].resid_norm > target * (1 + 1e-3)
+
+
+def test_p10_duplicate_column_is_degenerate():
+    A = _gauss(16, 12, 41)
+    A[:, 5] = A[:, 2]                       # exact duplicate atom
+    y = 2.0 * A[:, 2] + 0.5 * A[:, 7]
+    r = omp(A, y, 6)
+    assert r.status == DEGENERATE
+    assert set(r.support) == {2, 7}
+    assert r.n_iter == 2
+
+
+def test_p10_nan_signal_and_bad_dictionary():
+    A = _gauss(8, 16, 5)
+    y = np.ones(8)
+    y[3] = np.nan
+    r = omp(A, y, 3)
+    assert r.status == NAN and r.n_iter == 0
+    Az = A.copy()
+    Az[:, 4] = 0
+    with pytest.raises(ValueError, match="column 4"):
+        omp(Az, np.ones(8), 2)
+    An = A.copy()
+    An[2, 9] = np.inf
+    with pytest.raises(ValueError, match="column 9"):
+        omp(An, np.ones(8), 2)
+
+
+def test_c3_noise_eps_stops_sample():
+    prob = make_problem("c3", B=2)
+    for y in prob.Y:
+        r = omp(prob.A, y, prob.S, prob.eps)
+        assert r.status == EPS and r.resid_norm <= prob.eps
+        assert all(s.resid_norm > prob.eps for s in r.steps[:-1])
+        assert 8 <= r.n_iter <= prob.S
