@@ -1,0 +1,469 @@
+// Host orchestrator + C ABI (include/omp_b200.h).
+//
+// One ompBatch = batch init (a1) followed by S iterations of
+//   K1 correlation (a2) -> K2 select (a3) -> K3 factor append (a4) -> K4 residual (a5)
+// all stream-ordered on the caller's stream with no host synchronisation inside the loop
+// (SURVEY §3 "Ours", stack 2).  Finished signals keep their captured result and skip
+// K2-K4 (capture-and-continue).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <climits>
+#include <new>
+#include <vector>
+
+#include "omp_internal.cuh"
+
+using namespace ompb;
+
+struct ProfRec {
+  int slot;
+  cudaEvent_t a, b;
+};
+
+struct ompHandle_st {
+  int device = 0;
+  int64_t M = 0, N = 0, Mp = 0, Np = 0;
+  int mode = OMP_CORR_3XTF32;
+  // dictionary (owned): FP32 copy and TF32 planes of A^T (Np x Mp), 1/||a_n||, Gram (Np x Np)
+  float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *inv_norm = nullptr, *G = nullptr;
+  int* dflags = nullptr;
+  // batch workspace
+  int64_t capB = 0;
+  int32_t capS = 0;
+  float *R_hi = nullptr, *R_lo = nullptr, *C = nullptr, *P0 = nullptr, *F = nullptr, *U = nullptr;
+  int32_t* nstar = nullptr;
+  int64_t ldf = 0, ldu = 0;
+  int64_t lastB = 0;
+  int32_t lastS = 0;
+  // host-call staging
+  int64_t capHB = 0;
+  int32_t capHS = 0;
+  float *hY = nullptr, *hX = nullptr, *hres = nullptr;
+  int32_t *hsup = nullptr, *hnit = nullptr, *hst = nullptr;
+  // diagnostics
+  int64_t err_detail = 0;
+  int64_t last_launches = 0;
+  bool profile = false;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[OMP_NUM_KERNEL_SLOTS] = {0};
+  int64_t prof_n[OMP_NUM_KERNEL_SLOTS] = {0};
+};
+
+static thread_local int64_t g_create_detail = 0;
+
+namespace {
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+static void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+template <typename T>
+static bool dalloc(T*& p, size_t count) {
+  dfree(p);
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)) == cudaSuccess;
+}
+
+static ompStatus_t cuda_fail(ompHandle_t h, cudaError_t e) {
+  if (h) h->err_detail = (int64_t)e;
+  else g_create_detail = (int64_t)e;
+  cudaGetLastError();   // clear sticky-free errors
+  return OMP_ERR_CUDA;
+}
+
+static cudaEvent_t take_event(ompHandle_t h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// K1 dispatch: no silent fallback between modes
+static cudaError_t corr(ompHandle_t h, const Planes& R, float* C, int64_t ldc, cudaStream_t st) {
+  Planes At{h->At_hi, h->At_lo, h->Np, h->Mp};
+  if (h->mode == OMP_CORR_3XTF32) return launch_corr_tc(R, At, h->Mp, C, ldc, st);
+  return launch_corr_simt(R, At, h->Mp, C, ldc, st);
+}
+
+struct Launcher {
+  ompHandle_t h;
+  cudaStream_t st;
+  int64_t count = 0;
+  cudaEvent_t a = nullptr;
+  void begin(int slot) {
+    (void)slot;
+    if (h->profile) {
+      a = take_event(h);
+      cudaEventRecord(a, st);
+    }
+  }
+  void end(int slot) {
+    ++count;
+    if (h->profile) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, st);
+      h->prof_pending.push_back({slot, a, b});
+    }
+  }
+};
+
+static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
+  if (B <= h->capB && S <= h->capS) return OMP_OK;
+  const int64_t nB = B > h->capB ? B : h->capB;
+  const int32_t nS = S > h->capS ? S : h->capS;
+  const int64_t ldf = (int64_t)nS * (nS + 1) / 2;
+  bool ok = dalloc(h->R_hi, (size_t)nB * h->Mp) && dalloc(h->R_lo, (size_t)nB * h->Mp) &&
+            dalloc(h->C, (size_t)nB * h->Np) && dalloc(h->P0, (size_t)nB * h->Np) &&
+            dalloc(h->F, (size_t)nB * ldf) && dalloc(h->U, (size_t)nB * nS) &&
+            dalloc(h->nstar, (size_t)nB);
+  if (!ok) {
+    dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->P0); dfree(h->F); dfree(h->U);
+    dfree(h->nstar);
+    h->capB = 0;
+    h->capS = 0;
+    cudaGetLastError();
+    return OMP_ERR_NOMEM;
+  }
+  h->capB = nB;
+  h->capS = nS;
+  h->ldf = ldf;
+  h->ldu = nS;
+  return OMP_OK;
+}
+
+static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
+                             float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
+                             float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
+  ompStatus_t s = ensure_workspace(h, B, S);
+  if (s != OMP_OK) return s;
+  if (!(eps >= 0.f)) eps = -1.f;   // NaN or negative: no tolerance
+  Launcher L{h, st};
+  cudaError_t e;
+  L.begin(0);
+  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, h->R_hi, h->R_lo, X, ldx, support, lds,
+                        resid, n_iter, status, st);
+  L.end(0);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  Planes R{h->R_hi, h->R_lo, B, h->Mp};
+  for (int32_t k = 0; k < S; ++k) {
+    // a2: C = A^T R_k (k = 0: R_0 = Y, kept as P0 = A^T Y for the beta = a_{n*}^T y lookups)
+    float* Ck = (k == 0) ? h->P0 : h->C;
+    L.begin(1);
+    e = corr(h, R, Ck, h->Np, st);
+    L.end(1);
+    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(2);
+    e = launch_select(Ck, h->Np, B, h->N, h->inv_norm, status, h->nstar, st);
+    L.end(2);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(3);
+    e = launch_factor_append(k, B, h->nstar, h->G, h->Np, h->P0, h->Np, h->F, h->ldf, h->U, h->ldu,
+                             X, ldx, support, lds, status, st);
+    L.end(3);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(4);
+    e = launch_residual(k, S, eps, B, Y, ldy, h->M, h->Mp, h->At, X, ldx, support, lds, h->R_hi,
+                        h->R_lo, resid, n_iter, status, st);
+    L.end(4);
+    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  }
+  h->last_launches = L.count;
+  h->lastB = B;
+  h->lastS = S;
+  return OMP_OK;
+}
+
+static ompStatus_t check_batch_args(ompHandle_t h, const void* Y, int64_t B, int64_t ldy, int32_t S,
+                                    const void* X, int64_t ldx, const void* support, int64_t lds,
+                                    const void* resid, const void* n_iter, const void* status) {
+  if (!h || B < 0 || ldy < h->M) return OMP_ERR_INVALID_ARG;
+  if (S < 1 || S > h->M || S > h->N) return OMP_ERR_INVALID_ARG;
+  if (S > MAX_S) return OMP_ERR_UNSUPPORTED;
+  if (ldx < S || lds < S) return OMP_ERR_INVALID_ARG;
+  if (B > 0 && (!Y || !X || !support || !resid || !n_iter || !status)) return OMP_ERR_INVALID_ARG;
+  if (h->Mp > 8192) return OMP_ERR_UNSUPPORTED;
+  return OMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ompGetErrorString(ompStatus_t s) {
+  switch (s) {
+    case OMP_OK: return "OMP_OK";
+    case OMP_ERR_INVALID_ARG: return "OMP_ERR_INVALID_ARG: invalid argument";
+    case OMP_ERR_ZERO_COLUMN: return "OMP_ERR_ZERO_COLUMN: dictionary column with zero norm";
+    case OMP_ERR_NONFINITE: return "OMP_ERR_NONFINITE: non-finite entry in the dictionary";
+    case OMP_ERR_NOMEM: return "OMP_ERR_NOMEM: device allocation failed";
+    case OMP_ERR_CUDA: return "OMP_ERR_CUDA: CUDA call failed";
+    case OMP_ERR_UNSUPPORTED: return "OMP_ERR_UNSUPPORTED: shape or mode not supported";
+  }
+  return "unknown ompStatus_t";
+}
+
+int64_t ompGetErrorDetail(ompHandle_t h) { return h ? h->err_detail : g_create_detail; }
+
+int64_t ompGetLaunchCount(ompHandle_t h) { return h ? h->last_launches : 0; }
+
+ompStatus_t ompDestroy(ompHandle_t h) {
+  if (!h) return OMP_ERR_INVALID_ARG;
+  {
+    DevGuard g(h->device);
+    cudaDeviceSynchronize();
+    dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->inv_norm); dfree(h->G);
+    dfree(h->dflags);
+    dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->P0); dfree(h->F); dfree(h->U);
+    dfree(h->nstar);
+    dfree(h->hY); dfree(h->hX); dfree(h->hres); dfree(h->hsup); dfree(h->hnit); dfree(h->hst);
+    for (auto& r : h->prof_pending) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+  }
+  delete h;
+  return OMP_OK;
+}
+
+ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, int64_t N, int64_t lda,
+                      int corr_mode, void* stream) {
+  if (!out) return OMP_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!A || M < 1 || N < 1 || lda < M) return OMP_ERR_INVALID_ARG;
+  if (corr_mode != OMP_CORR_3XTF32 && corr_mode != OMP_CORR_FP32_SIMT) return OMP_ERR_INVALID_ARG;
+  if (N > INT_MAX / 2) return OMP_ERR_UNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return OMP_ERR_INVALID_ARG;
+  }
+  DevGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  ompHandle_t h = new (std::nothrow) ompHandle_st();
+  if (!h) return OMP_ERR_NOMEM;
+  h->device = device;
+  h->M = M;
+  h->N = N;
+  h->Mp = round_up(M, K_TILE);
+  h->Np = round_up(N, N_TILE);
+  h->mode = corr_mode;
+  const size_t plane = (size_t)h->Np * h->Mp;
+  if (!(dalloc(h->At, plane) && dalloc(h->At_hi, plane) && dalloc(h->At_lo, plane) &&
+        dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
+        dalloc(h->dflags, 2))) {
+    ompDestroy(h);
+    cudaGetLastError();
+    return OMP_ERR_NOMEM;
+  }
+  int init_flags[2] = {INT_MAX, INT_MAX};
+  cudaError_t e = cudaMemcpyAsync(h->dflags, init_flags, sizeof(init_flags), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->At_hi, h->At_lo, h->inv_norm,
+                             h->dflags, h->dflags + 1, st);
+  int flags[2] = {INT_MAX, INT_MAX};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(flags, h->dflags, sizeof(flags), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    ompStatus_t s = cuda_fail(nullptr, e);
+    ompDestroy(h);
+    return s;
+  }
+  if (flags[1] != INT_MAX || flags[0] != INT_MAX) {
+    const bool nonfinite = flags[1] != INT_MAX;
+    g_create_detail = nonfinite ? flags[1] : flags[0];
+    ompDestroy(h);
+    return nonfinite ? OMP_ERR_NONFINITE : OMP_ERR_ZERO_COLUMN;
+  }
+  // Gram matrix G = A^T A through the correlation kernel itself (R := A^T)
+  Planes R{h->At_hi, h->At_lo, h->Np, h->Mp};
+  e = corr(h, R, h->G, h->Np, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    const bool unsup = e == cudaErrorNotSupported;
+    ompStatus_t s = unsup ? OMP_ERR_UNSUPPORTED : cuda_fail(nullptr, e);
+    ompDestroy(h);
+    return s;
+  }
+  *out = h;
+  return OMP_OK;
+}
+
+ompStatus_t ompBatch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S, float eps, float* X,
+                     int64_t ldx, int32_t* support, int64_t lds, float* resid, int32_t* n_iter,
+                     int32_t* status, void* stream) {
+  ompStatus_t s = check_batch_args(h, Y, B, ldy, S, X, ldx, support, lds, resid, n_iter, status);
+  if (s != OMP_OK) return s;
+  if (B == 0) return OMP_OK;
+  DevGuard g(h->device);
+  return run_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status,
+                   (cudaStream_t)stream);
+}
+
+ompStatus_t ompBatchHost(ompHandle_t h, const float* Yh, int64_t B, int64_t ldy, int32_t S, float eps,
+                         float* Xh, int64_t ldx, int32_t* suph, int64_t lds, float* resh, int32_t* nith,
+                         int32_t* sth, void* stream) {
+  ompStatus_t s = check_batch_args(h, Yh, B, ldy, S, Xh, ldx, suph, lds, resh, nith, sth);
+  if (s != OMP_OK) return s;
+  if (B == 0) return OMP_OK;
+  DevGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (B > h->capHB || S > h->capHS) {
+    const int64_t nB = B > h->capHB ? B : h->capHB;
+    const int32_t nS = S > h->capHS ? S : h->capHS;
+    if (!(dalloc(h->hY, (size_t)nB * h->M) && dalloc(h->hX, (size_t)nB * nS) &&
+          dalloc(h->hsup, (size_t)nB * nS) && dalloc(h->hres, (size_t)nB) &&
+          dalloc(h->hnit, (size_t)nB) && dalloc(h->hst, (size_t)nB))) {
+      h->capHB = 0;
+      h->capHS = 0;
+      cudaGetLastError();
+      return OMP_ERR_NOMEM;
+    }
+    h->capHB = nB;
+    h->capHS = nS;
+  }
+  cudaError_t e = cudaMemcpy2DAsync(h->hY, h->M * sizeof(float), Yh, ldy * sizeof(float),
+                                    h->M * sizeof(float), B, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  s = run_batch(h, h->hY, B, h->M, S, eps, h->hX, S, h->hsup, S, h->hres, h->hnit, h->hst, st);
+  if (s != OMP_OK) return s;
+  e = cudaMemcpy2DAsync(Xh, ldx * sizeof(float), h->hX, S * sizeof(float), S * sizeof(float), B,
+                        cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(suph, lds * sizeof(int32_t), h->hsup, S * sizeof(int32_t),
+                          S * sizeof(int32_t), B, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(resh, h->hres, B * sizeof(float), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(nith, h->hnit, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sth, h->hst, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  return OMP_OK;
+}
+
+ompStatus_t ompDensify(ompHandle_t h, const float* X, int64_t ldx, const int32_t* support, int64_t lds,
+                       const int32_t* n_iter, int64_t B, int32_t S, float* Xd, int64_t ldxd, void* stream) {
+  if (!h || B < 0 || S < 1 || ldx < S || lds < S || ldxd < h->N) return OMP_ERR_INVALID_ARG;
+  if (B == 0) return OMP_OK;
+  if (!X || !support || !n_iter || !Xd) return OMP_ERR_INVALID_ARG;
+  DevGuard g(h->device);
+  cudaError_t e = launch_densify(X, ldx, support, lds, n_iter, B, S, h->N, Xd, ldxd, (cudaStream_t)stream);
+  return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
+}
+
+ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, float* C, int64_t ldc,
+                         void* stream) {
+  if (!h || B < 0 || ldr < h->M || ldc < h->N) return OMP_ERR_INVALID_ARG;
+  if (B == 0) return OMP_OK;
+  if (!R || !C) return OMP_ERR_INVALID_ARG;
+  DevGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  ompStatus_t s = ensure_workspace(h, B, h->capS > 0 ? h->capS : 1);
+  if (s != OMP_OK) return s;
+  cudaError_t e = launch_split_rows(R, B, ldr, h->M, h->Mp, h->R_hi, h->R_lo, st);
+  Planes P{h->R_hi, h->R_lo, B, h->Mp};
+  if (e == cudaSuccess) e = corr(h, P, h->C, h->Np, st);
+  if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(C, ldc * sizeof(float), h->C, h->Np * sizeof(float), h->N * sizeof(float), B,
+                          cudaMemcpyDeviceToDevice, st);
+  return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
+}
+
+ompStatus_t ompGetGram(ompHandle_t h, float* G, int64_t ldg, void* stream) {
+  if (!h || !G || ldg < h->N) return OMP_ERR_INVALID_ARG;
+  DevGuard g(h->device);
+  cudaError_t e = cudaMemcpy2DAsync(G, ldg * sizeof(float), h->G, h->Np * sizeof(float),
+                                    h->N * sizeof(float), h->N, cudaMemcpyDeviceToDevice,
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
+}
+
+ompStatus_t ompGetFactor(ompHandle_t h, int64_t b0, int64_t count, float* F, float* u, void* stream) {
+  if (!h || b0 < 0 || count < 0 || b0 + count > h->lastB || h->lastS < 1) return OMP_ERR_INVALID_ARG;
+  if (count == 0) return OMP_OK;
+  DevGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t S = h->lastS, pf = S * (S + 1) / 2;
+  cudaError_t e = cudaSuccess;
+  if (F)
+    e = cudaMemcpy2DAsync(F, pf * sizeof(float), h->F + b0 * h->ldf, h->ldf * sizeof(float),
+                          pf * sizeof(float), count, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && u)
+    e = cudaMemcpy2DAsync(u, S * sizeof(float), h->U + b0 * h->ldu, h->ldu * sizeof(float),
+                          S * sizeof(float), count, cudaMemcpyDeviceToDevice, st);
+  return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
+}
+
+ompStatus_t ompProfileEnable(ompHandle_t h, int enable) {
+  if (!h) return OMP_ERR_INVALID_ARG;
+  h->profile = enable != 0;
+  return OMP_OK;
+}
+
+ompStatus_t ompProfileRead(ompHandle_t h, double* ms, int64_t* launches, int reset) {
+  if (!h) return OMP_ERR_INVALID_ARG;
+  DevGuard g(h->device);
+  for (auto& r : h->prof_pending) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    h->prof_ms[r.slot] += t;
+    h->prof_n[r.slot] += 1;
+    h->ev_pool.push_back(r.a);
+    h->ev_pool.push_back(r.b);
+  }
+  h->prof_pending.clear();
+  for (int i = 0; i < OMP_NUM_KERNEL_SLOTS; ++i) {
+    if (ms) ms[i] = h->prof_ms[i];
+    if (launches) launches[i] = h->prof_n[i];
+    if (reset) {
+      h->prof_ms[i] = 0;
+      h->prof_n[i] = 0;
+    }
+  }
+  return OMP_OK;
+}
+
+ompStatus_t omp_batch(const float* A, int64_t M, int64_t N, const float* Y, int64_t B, int32_t S, float eps,
+                      float* X, int32_t* support, float* resid, int32_t* n_iter, int32_t* status,
+                      void* stream) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(nullptr, cudaGetLastError());
+  ompHandle_t h = nullptr;
+  ompStatus_t s = ompCreate(&h, dev, A, M, N, M, OMP_CORR_3XTF32, stream);
+  if (s != OMP_OK) return s;
+  s = ompBatch(h, Y, B, M, S, eps, X, S, support, S, resid, n_iter, status, stream);
+  if (s == OMP_OK) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) s = cuda_fail(nullptr, e);
+  }
+  ompDestroy(h);
+  return s;
+}
+
+}  // extern "C"

@@ -79,23 +79,56 @@ def _draw_signal(b: int, seed: int, N: int, M: int, sparsity: Sparsity, sigma: f
 
 
 def make_signals(A32: np.ndarray, indices: Sequence[int], seed: int, sparsity: Sparsity,
-                 sigma: float = 0.0, with_truth: bool = False):
-    """Signals y_b for the given signal indices, as an FP32 array of shape (len(indices), M)."""
+                 sigma: float = 0.0, with_truth: bool = False, device=None):
+    """Signals y_b for the given signal indices, as an FP32 array of shape (len(indices), M).
+
+    ``device`` (e.g. "cuda:0") forms the FP64 sums y = A x + noise with torch on that
+    device instead of numpy (same draws, FP64 either way; only the summation order of
+    the FP64 sum differs, which can move an FP32-rounded entry by one ulp).  Used for
+    the 1e5-1e6-signal configs, where the numpy gather would take minutes.
+    """
     M, N = A32.shape
-    AT64 = np.ascontiguousarray(A32.T, dtype=np.float64)  # atom rows, FP64 copy of the FP32 values
     idx = np.asarray(indices, dtype=np.int64)
-    Y = np.empty((idx.size, M), dtype=np.float32)
-    truth = Truth() if with_truth else None
-    for i, b in enumerate(idx):
-        supp, coef, noise = _draw_signal(int(b), seed, N, M, sparsity, sigma)
-        y = coef @ AT64[supp]
-        if noise is not None:
-            y = y + noise
-        Y[i] = y.astype(np.float32)
-        if truth is not None:
-            truth.supports.append(supp)
-            truth.coefs.append(coef)
+    draws = [_draw_signal(int(b), seed, N, M, sparsity, sigma) for b in idx]
+    truth = None
+    if with_truth:
+        truth = Truth([d[0] for d in draws], [d[1] for d in draws])
+    if device is None:
+        AT64 = np.ascontiguousarray(A32.T, dtype=np.float64)  # atom rows, FP64 copy of the FP32 values
+        Y = np.empty((idx.size, M), dtype=np.float32)
+        for i, (supp, coef, noise) in enumerate(draws):
+            y = coef @ AT64[supp]
+            if noise is not None:
+                y = y + noise
+            Y[i] = y.astype(np.float32)
+    else:
+        Y = _signals_torch(A32, draws, M, device)
     return (Y, truth) if with_truth else Y
+
+
+def _signals_torch(A32, draws, M, device, chunk=512):
+    import torch
+    AT64 = torch.from_numpy(np.ascontiguousarray(A32.T)).to(device=device, dtype=torch.float64)
+    B = len(draws)
+    smax = max((len(d[0]) for d in draws), default=0)
+    supp = np.zeros((B, smax), np.int64)
+    coef = np.zeros((B, smax), np.float64)      # zero-padded coefficients add exact zeros
+    noise = np.zeros((B, M), np.float64) if any(d[2] is not None for d in draws) else None
+    for i, (s, c, nz) in enumerate(draws):
+        supp[i, :len(s)] = s
+        coef[i, :len(c)] = c
+        if nz is not None:
+            noise[i] = nz
+    out = np.empty((B, M), np.float32)
+    for a in range(0, B, chunk):
+        e = min(B, a + chunk)
+        sp = torch.from_numpy(supp[a:e]).to(device)
+        cf = torch.from_numpy(coef[a:e]).to(device)
+        y = torch.bmm(cf[:, None, :], AT64[sp])[:, 0, :]
+        if noise is not None:
+            y = y + torch.from_numpy(noise[a:e]).to(device)
+        out[a:e] = y.to(torch.float32).cpu().numpy()
+    return out
 
 
 @dataclass
@@ -123,12 +156,13 @@ class Problem:
 
 
 def make_problem(name: str, B: Optional[int] = None, indices: Optional[Sequence[int]] = None,
-                 with_truth: bool = False, **overrides) -> Problem:
+                 with_truth: bool = False, device=None, **overrides) -> Problem:
     cfg = config(name, **overrides)
     if indices is None:
         indices = np.arange(cfg["B"] if B is None else B)
     A = make_dictionary(cfg["M"], cfg["N"], cfg["seed"])
-    out = make_signals(A, indices, cfg["seed"], cfg["sparsity"], cfg["sigma"], with_truth=with_truth)
+    out = make_signals(A, indices, cfg["seed"], cfg["sparsity"], cfg["sigma"], with_truth=with_truth,
+                       device=device)
     Y, truth = out if with_truth else (out, None)
     return Problem(name=name, A=A, Y=Y, S=cfg["S"], eps=cfg["eps"], seed=cfg["seed"],
                    indices=np.asarray(indices, dtype=np.int64), truth=truth)

@@ -1,0 +1,47 @@
+"""Shared helpers for the -m gpu tests: run the CUDA path through the C ABI, run the oracle,
+compare with the parity protocol."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import omp_batch as oracle_batch
+from parity import compare_batch
+
+
+def eps32(eps):
+    """The tolerance exactly as the library receives it (an FP32 scalar)."""
+    return None if eps is None else float(np.float32(eps))
+
+
+def run_gpu(A_np, Y_np, S, eps=None, mode="3xtf32", handle=None):
+    import torch
+    from paper_2407_06434_b200 import OMP
+    A = torch.from_numpy(A_np).cuda()
+    Y = torch.from_numpy(np.ascontiguousarray(Y_np)).cuda()
+    own = handle is None
+    h = OMP(A, mode=mode) if own else handle
+    try:
+        res = h.batch(Y, S, eps32(eps))
+        torch.cuda.synchronize()
+        out = dict(support=res.support.cpu().numpy(), X=res.X.cpu().numpy(),
+                   resid=res.resid_norm.cpu().numpy(), n_iter=res.n_iter.cpu().numpy(),
+                   status=res.status.cpu().numpy(), launches=h.launch_count())
+    finally:
+        if own:
+            h.close()
+    return out
+
+
+def parity(out, A_np, Y_np, S, eps, rows, workers=None):
+    rows = list(rows)
+    ora = oracle_batch(A_np, Y_np[rows], S, eps32(eps), workers=workers)
+    return compare_batch(out["support"], out["X"], out["resid"], out["n_iter"], out["status"], ora,
+                         A_np.shape[1], rows=rows)
+
+
+def assert_no_bugs(rep, label=""):
+    d = rep.as_dict()
+    print(f"parity {label}: {d}")
+    assert rep.counts.get("bug", 0) == 0, d
+    return d

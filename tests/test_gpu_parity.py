@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the FP64 oracle on the same seeded inputs.
+
+Protocol and tolerances: tests/parity.py (BASELINE.json north_star):
+supports bit-exact outside oracle-flagged near-ties, coefficients <= 1e-4 relative L2,
+residual norms <= 1e-4 relative (+1e-5 ||y|| floor, reading R10).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from gpu_helpers import assert_no_bugs, eps32, parity, run_gpu
+from oracle import DEGENERATE, EPS, MAXITER, NAN
+from synth import make_dictionary, make_problem, make_signals
+
+pytestmark = pytest.mark.gpu
+MODES = ["3xtf32", "simt"]
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
+
+
+# ------------------------------------------------------------------ correlation GEMM (K1)
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", [(32, 64, 16), (256, 1024, 1000), (300, 700, 333), (1024, 4096, 520)])
+def test_correlation_gemm_vs_fp64(mode, shape):
+    import torch
+    from paper_2407_06434_b200 import OMP
+    M, N, B = shape
+    rng = np.random.default_rng(M + N + B)
+    A = rng.standard_normal((M, N)).astype(np.float32)
+    R = rng.standard_normal((B, M)).astype(np.float32)
+    with OMP(torch.from_numpy(A).cuda(), mode=mode) as h:
+        C = h.correlate(torch.from_numpy(R).cuda()).cpu().numpy()
+        G = h.gram().cpu().numpy()
+    ref = R.astype(np.float64) @ A.astype(np.float64)
+    scale = np.linalg.norm(R, axis=1)[:, None] * np.linalg.norm(A, axis=0)[None, :]
+    err = np.abs(C - ref) / scale
+    print(f"{mode} {shape}: max |C - C64| / (|r||a|) = {err.max():.3e}")
+    assert err.max() <= 1e-6
+    A64 = A.astype(np.float64)
+    Gref = A64.T @ A64
+    gs = np.linalg.norm(A, axis=0)
+    gerr = np.abs(G - Gref) / (gs[:, None] * gs[None, :])
+    assert gerr.max() <= 1e-6
+
+
+# ------------------------------------------------------------------ worked examples (P5) on the GPU
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("ex", GOLD["omp"], ids=[e["name"] for e in GOLD["omp"]])
+def test_worked_examples_gpu(mode, ex):
+    A = np.array(ex["A_columns"], dtype=np.float32).T.copy()
+    y = np.array([ex["y"]], dtype=np.float32)
+    out = run_gpu(A, y, ex["S"], ex.get("eps"), mode)
+    e = ex["expect"]
+    k = len(e["support"])
+    assert out["status"][0] == STATUS[e["status"]]
+    assert out["n_iter"][0] == k
+    assert list(out["support"][0][:k]) == e["support"]
+    assert np.all(out["support"][0][k:] == -1)
+    np.testing.assert_allclose(out["X"][0][:k], e["x"], atol=1e-6)
+    assert np.all(out["X"][0][k:] == 0)
+
+
+# ------------------------------------------------------------------ configs
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_tiny(mode):
+    prob = make_problem("tiny")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
+    rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, range(prob.B))
+    d = assert_no_bugs(rep, f"tiny/{mode}")
+    assert d["counts"].get("exact", 0) == prob.B
+    assert out["launches"] == 1 + 4 * prob.S
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c2_all(mode):
+    prob = make_problem("c2")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
+    rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, range(prob.B))
+    d = assert_no_bugs(rep, f"c2/{mode}")
+    assert d["counts"].get("exact", 0) + d["counts"].get("flagged_ok", 0) >= 995
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c3_full_batch_sampled(mode):
+    prob = make_problem("c3", device="cuda")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
+    rows = np.unique(np.r_[np.arange(0, 96), np.linspace(0, prob.B - 1, 96).astype(int), prob.B - 1])
+    rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, rows)
+    assert_no_bugs(rep, f"c3/{mode}")
+    st = out["status"]
+    assert np.mean(st == EPS) > 0.95            # c3 stops by eps
+
+
+@pytest.mark.parametrize("B", [1, 10, 1000, 100000])
+def test_parity_c5_sweep_sampled(B):
+    prob = make_problem("c5", B=B, device="cuda" if B > 1000 else None)
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "3xtf32")
+    rows = np.unique(np.linspace(0, B - 1, min(B, 48)).astype(int))
+    assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), f"c5 B={B}")
+
+
+def test_parity_c4_full_batch_sampled():
+    """BASELINE.json's largest config at its full size (B = 1e5), the bench's launch configuration."""
+    prob = make_problem("c4", device="cuda")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "3xtf32")
+    rows = [0, 1, 12499, 12500, 49999, 50000, 87499, 99999]
+    assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), "c4")
+    assert np.all(out["status"] == MAXITER) and np.all(out["n_iter"] == prob.S)
+
+
+# ------------------------------------------------------------------ ragged shapes, edge cases
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("MNBS", [(33, 77, 5, 7), (100, 300, 129, 20), (257, 513, 257, 31)])
+def test_ragged_shapes(mode, MNBS):
+    M, N, B, S = MNBS
+    A = make_dictionary(M, N, 17)
+    Y = make_signals(A, range(B), 17, max(2, S // 2), sigma=0.01)
+    out = run_gpu(A, Y, S, None, mode)
+    assert_no_bugs(parity(out, A, Y, S, None, range(B)), f"ragged {MNBS}/{mode}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_edge_cases(mode):
+    A = make_dictionary(64, 128, 5)
+    A[:, 9] = A[:, 3]                       # duplicate atom -> DEGENERATE after exhaustion
+    Y = make_signals(A, range(6), 5, 3)
+    Y[1] = 0.0                              # zero signal: eps=0 stops at k = 0
+    Y[2, 7] = np.nan                        # NaN signal
+    Y[3] = 2.0 * A[:, 3] - A[:, 50]         # exactly 2-sparse with a duplicated atom
+    yn = np.linalg.norm(Y[4].astype(np.float64))
+    # eps >= ||y_4|| stops before the first selection; others keep going
+    out = run_gpu(A, Y, 8, 0.0, mode)
+    assert out["status"][1] == EPS and out["n_iter"][1] == 0 and np.all(out["support"][1] == -1)
+    assert out["status"][2] == NAN and out["n_iter"][2] == 0
+    assert out["status"][3] in (DEGENERATE, MAXITER)
+    assert set(out["support"][3][:2]) == {3, 50}
+    out = run_gpu(A, Y[4:5], 8, float(yn) * 1.0001, mode)
+    assert out["status"][0] == EPS and out["n_iter"][0] == 0
+    assert out["resid"][0] == pytest.approx(yn, rel=1e-6)
+
+
+def test_invalid_dictionary_and_args():
+    import torch
+    from paper_2407_06434_b200 import OMP, OmpError
+    A = make_dictionary(16, 32, 1)
+    A[:, 7] = 0.0
+    with pytest.raises(OmpError) as ei:
+        OMP(torch.from_numpy(A).cuda())
+    assert ei.value.status == 2 and ei.value.detail == 7
+    A[:, 7] = 1.0
+    A[3, 11] = np.inf
+    with pytest.raises(OmpError) as ei:
+        OMP(torch.from_numpy(A).cuda())
+    assert ei.value.status == 3 and ei.value.detail == 11
+    A = make_dictionary(16, 32, 1)
+    with OMP(torch.from_numpy(A).cuda()) as h:
+        Y = torch.zeros((3, 16), device="cuda")
+        with pytest.raises(OmpError):
+            h.batch(Y, 17)                   # S > M
+        with pytest.raises(OmpError):
+            h.batch(Y, 0)
+        r = h.batch(Y[:0], 4)                # B = 0 is a no-op
+        assert r.X.shape == (0, 4)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_batch_invariance_bitwise(mode):
+    """P8: signal b's result does not depend on B or on its position (no split-K in K1)."""
+    prob = make_problem("c2", B=300)
+    full = run_gpu(prob.A, prob.Y, prob.S, None, mode)
+    part = run_gpu(prob.A, prob.Y[130:260], prob.S, None, mode)
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(full[key][130:260], part[key]), key
+
+
+def test_host_path_matches_device_path():
+    import torch
+    from paper_2407_06434_b200 import OMP
+    prob = make_problem("c2", B=200)
+    with OMP(torch.from_numpy(prob.A).cuda()) as h:
+        dev = h.batch(torch.from_numpy(prob.Y).cuda(), prob.S)
+        host = h.batch_host(prob.Y, prob.S)
+        torch.cuda.synchronize()
+        assert np.array_equal(dev.support.cpu().numpy(), host.support)
+        assert np.array_equal(dev.X.cpu().numpy(), host.X)
+        assert np.array_equal(dev.resid_norm.cpu().numpy(), host.resid_norm)
+        Xd = h.densify(dev).cpu().numpy()
+    sup = host.support
+    for b in range(5):
+        k = host.n_iter[b]
+        want = np.zeros(prob.N, np.float32)
+        want[sup[b, :k]] = host.X[b, :k]
+        assert np.array_equal(Xd[b], want)
+
+
+def test_inverse_cholesky_state_identity():
+    """P9 on the GPU's own factor: F_k V_k^T = I with V_k from numpy.linalg.cholesky."""
+    import torch
+    from paper_2407_06434_b200 import OMP
+    prob = make_problem("c2", B=4)
+    S = prob.S
+    with OMP(torch.from_numpy(prob.A).cuda()) as h:
+        res = h.batch(torch.from_numpy(prob.Y).cuda(), S)
+        F, u = h.factor(0, 4, S)
+        F, u = F.cpu().numpy(), u.cpu().numpy()
+        sup = res.support.cpu().numpy()
+    A64 = prob.A.astype(np.float64)
+    for b in range(4):
+        Fd = np.zeros((S, S))
+        for j in range(S):
+            Fd[:j + 1, j] = F[b, j * (j + 1) // 2: j * (j + 1) // 2 + j + 1]
+        A_k = A64[:, sup[b]]
+        V = np.linalg.cholesky(A_k.T @ A_k)
+        assert np.abs(Fd @ V.T - np.eye(S)).max() <= 5e-5
+        np.testing.assert_allclose(u[b], Fd.T @ (A_k.T @ prob.Y[b].astype(np.float64)), atol=2e-5)

@@ -59,3 +59,10 @@ def test_generator_contract():
     assert set(CONFIGS) == {"tiny", "c2", "c3", "c4", "c5"}
     p = make_problem("c3", B=3)
     assert p.eps is not None and abs(p.eps - 0.32) < 1e-12 and p.Y.shape == (3, 1024)
+
+
+def test_generator_torch_backend_matches_numpy():
+    A = make_dictionary(64, 256, 3)
+    Yn = make_signals(A, range(20), 3, (4, 9), sigma=0.01)
+    Yt = make_signals(A, range(20), 3, (4, 9), sigma=0.01, device="cpu")
+    np.testing.assert_allclose(Yt, Yn, rtol=2e-7, atol=1e-7)
