@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: batched OMP signals/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--mode bf16] [--impl ours|reference]
+
+A "step" is one ompBatch over the whole per-rank batch: S iterations of correlation screen,
+exact selection, factor append and residual on device-resident inputs.
+Multi-GPU (torchrun): the global batch of the config is sharded contiguously across ranks
+(BASELINE.json configs[3]: "B=100,000 batch-sharded across 1/2/4/8 B200"); A is generated on
+rank 0 and broadcast once over NCCL; there is no per-iteration collective.  Step time is the
+max over ranks of CUDA-event time (barrier + synchronize on both sides).
+
+`--impl reference` times the FP64 CPU oracle (the only reference this paper-tier run has) on a
+bounded sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "OMP signals/sec"
+UNIT = "signals/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c4")
+    p.add_argument("--batch", type=int, default=None, help="override the config's global batch")
+    p.add_argument("--mode", default="bf16", choices=["bf16", "3xtf32", "simt"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--oracle-sample", type=int, default=None, help="signals in the CPU oracle sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        busy = [v for v in sm if v > 0.5 * (max(mx) if mx else 0)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def ncu_traffic(kernel_key: str, config_name: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d["configs"][config_name][kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ roofline model
+def kernel_work(cfg, B):
+    """Algorithmic work per launch (per signal-iteration x the signals one launch covers)."""
+    M, N, S = cfg["M"], cfg["N"], cfg["S"]
+    k_avg = (S - 1) / 2.0
+    return {
+        # screen GEMM: 2 M N flops per signal-iteration (the FP32-equivalent contraction)
+        "correlation": ("tensor", 2.0 * M * N * B, "TFLOP/s"),
+        # refine: the fp32 residual row + ~2 candidate atom rows + partials
+        "select": ("hbm", B * (4.0 * M + 2 * 4.0 * M + 8.0 * 4 * math.ceil(N / 256)), "GB/s"),
+        # factor append: packed F read twice, new column write, Gram gathers
+        "factor_append": ("hbm", B * (2 * 4.0 * k_avg * (k_avg + 1) / 2 + 4.0 * (k_avg + 2) + 32.0 * k_avg), "GB/s"),
+        # residual: y read, fp32 + bf16 planes written, (k+1) atom rows gathered (L2)
+        "residual": ("hbm", B * (4.0 * M + 6.0 * M + 4.0 * (k_avg + 1) * M), "GB/s"),
+        "init": ("hbm", B * (4.0 * M + 6.0 * M), "GB/s"),
+    }
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    import torch
+    import torch.distributed as dist
+    from synth import config, make_dictionary, make_signals
+    from paper_2407_06434_b200 import OMP
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = config(args.config)
+    B_total = args.batch or cfg["B"]
+    per = -(-B_total // world)
+    lo, hi = rank * per, min(B_total, (rank + 1) * per)
+    B = max(0, hi - lo)
+    M, N, S, eps = cfg["M"], cfg["N"], cfg["S"], cfg["eps"]
+
+    # dictionary: generated on rank 0, broadcast once over NCCL (north star); signals: own shard
+    A_np = make_dictionary(M, N, cfg["seed"])
+    A = torch.from_numpy(A_np).to(dev) if rank == 0 else torch.empty((M, N), dtype=torch.float32, device=dev)
+    if world > 1:
+        dist.broadcast(A, src=0)
+    Y_np = make_signals(A.cpu().numpy(), range(lo, hi), cfg["seed"], cfg["sparsity"], cfg["sigma"], device=dev)
+    Y = torch.from_numpy(Y_np).to(dev)
+    eps32 = None if eps is None else float(np.float32(eps))
+
+    h = OMP(A, mode=args.mode)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        res = h.batch(Y, S, eps32)
+    torch.cuda.synchronize()
+
+    # timed region: per-kernel CUDA events inside the library (profiling mode) + step events
+    h.profile(True)
+    h.profile_read(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms = []
+    launches = 0
+    for _ in range(args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = h.batch(Y, S, eps32)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+        launches += h.launch_count()
+    clk = clocks.stop()
+    kern = h.profile_read(reset=True)
+    h.profile(False)
+    ms = statistics.mean(step_ms)
+    value = B_total / (ms / 1e3)
+
+    # end to end through the public host API: pinned host Y in, host results out, every step
+    e2e = None
+    if not args.no_e2e and B > 0:
+        Yh = torch.from_numpy(Y_np).pin_memory()
+        outs = (torch.empty((B, S), dtype=torch.float32).pin_memory().numpy(),
+                torch.empty((B, S), dtype=torch.int32).pin_memory().numpy(),
+                torch.empty((B,), dtype=torch.float32).pin_memory().numpy(),
+                torch.empty((B,), dtype=torch.int32).pin_memory().numpy(),
+                torch.empty((B,), dtype=torch.int32).pin_memory().numpy())
+        h.batch_host(Yh.numpy(), S, eps32, out=outs)   # warm the staging buffers
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            h.batch_host(Yh.numpy(), S, eps32, out=outs)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            e2e_ms.append(max_over_ranks(t0.elapsed_time(t1)))
+        e2e = {"value": B_total / (statistics.mean(e2e_ms) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(Y_np.nbytes) * world,
+               "d2h_bytes_per_step": int(sum(o.nbytes for o in outs)) * world}
+
+    # roofline of the dominant kernel (events measured live over the timed steps, this rank)
+    work = kernel_work(cfg, B)
+    dom = max((k for k in kern if k in work), key=lambda k: kern[k][0])
+    bound, per_launch, unit = work[dom]
+    t_launch = kern[dom][0] / max(1, kern[dom][1]) / 1e3
+    peaks = measured_peaks()
+    if bound == "tensor":
+        achieved = per_launch / t_launch / 1e12
+        if args.mode == "bf16":
+            peak, peak_src = ((peaks or {}).get("bf16_tflops_sustained", 1400.0),
+                              "MEASURED_PEAKS bf16_tflops_sustained" if peaks else "fallback 1.4 PF")
+        else:
+            base = (peaks or {}).get("bf16_tflops_sustained", 1400.0)
+            peak = base / 2.0 / (3.0 if args.mode == "3xtf32" else 1.0) if args.mode != "simt" else 74.0
+            peak_src = "bf16 sustained x nominal tf32/bf16 ratio 1/2 (/3 for 3 products)" if args.mode != "simt" \
+                else "FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz"
+    else:
+        achieved = per_launch / t_launch / 1e9
+        peak = (peaks or {}).get("hbm_gbs", 6650.0)
+        peak_src = "MEASURED_PEAKS hbm_gbs" if peaks else "fallback 6.65 TB/s"
+    roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak, "traffic": ncu_traffic(dom, args.config), "peak_source": peak_src,
+                "work_per_launch": per_launch, "launch_ms": t_launch * 1e3}
+    kernels = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / max(1e-9, sum(x[0] for x in kern.values()))}
+               for k, v in kern.items()}
+
+    # CPU baseline: the oracle on a bounded sample (rank 0, N = 1) + parity of that sample
+    cpu = None
+    parity_rep = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, parity_rep = cpu_baseline(args, cfg, A_np, Y_np, res, lo)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: M={M} N={N} S={S} B={B_total}"
+                                   + (f" sigma={cfg['sigma']} eps={eps:.4g}" if eps else " noiseless"),
+                       "M": M, "N": N, "S": S, "global_batch": B_total, "per_gpu_batch": per,
+                       "mode": args.mode, "screen_dtype": {"bf16": "bf16", "3xtf32": "tf32x3", "simt": "none"}[args.mode],
+                       "l2": "inputs larger than L2 (Y %.0f MB/rank)" % (Y_np.nbytes / 1e6),
+                       "parallelism": f"batch-shard x{world}"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "kernels": kernels,
+        }
+        if parity_rep is not None:
+            line["parity"] = parity_rep
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def oracle_sample_size(args, cfg, cores):
+    if args.oracle_sample:
+        return args.oracle_sample
+    per_signal_s = {"tiny": 3e-4, "c2": 0.012, "c3": 0.25, "c4": 3.4, "c5": 0.06}.get(cfg["name"], 1.0)
+    target = 20.0   # ~20 s of wall time on `cores` workers
+    return int(max(cores, min(4096, round(target * cores / per_signal_s))))
+
+
+def cpu_baseline(args, cfg, A_np, Y_np, res, lo):
+    from oracle import host_cores, omp_batch as oracle_batch
+    from parity import compare_batch
+    cores = host_cores()
+    n = min(len(Y_np), oracle_sample_size(args, cfg, cores))
+    rows = np.unique(np.linspace(0, len(Y_np) - 1, n).astype(int))
+    eps32 = None if cfg["eps"] is None else float(np.float32(cfg["eps"]))
+    t0 = time.perf_counter()
+    ora = oracle_batch(A_np, Y_np[rows], cfg["S"], eps32, workers=cores)
+    wall = time.perf_counter() - t0
+    cpu = {"value": len(rows) / wall, "unit": UNIT, "cores": min(cores, len(rows)), "kind": "oracle",
+           "sample": f"{len(rows)} signals of {cfg['name']} spread over the batch (rows {rows[0]}..{rows[-1]}), "
+                     f"FP64 numpy QR per step, one process per core, BLAS threads = 1; {wall:.1f} s wall"}
+    rep = compare_batch(res.support.cpu().numpy(), res.X.cpu().numpy(), res.resid_norm.cpu().numpy(),
+                        res.n_iter.cpu().numpy(), res.status.cpu().numpy(), ora, A_np.shape[1], rows=list(rows))
+    return cpu, rep.as_dict()
+
+
+def run_reference(args, world, rank):
+    """The reference arm: the FP64 CPU oracle as it stands, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import host_cores, omp_batch as oracle_batch
+    from synth import config, make_dictionary, make_signals
+    cfg = config(args.config)
+    B_total = args.batch or cfg["B"]
+    cores = host_cores()
+    n = oracle_sample_size(args, cfg, cores) if args.oracle_sample is None else args.oracle_sample
+    n = max(1, min(B_total, n // 2))   # each step is a bounded sample; keep the whole run ~minutes
+    A_np = make_dictionary(cfg["M"], cfg["N"], cfg["seed"])
+    eps32 = None if cfg["eps"] is None else float(np.float32(cfg["eps"]))
+    times = []
+    steps = max(1, args.steps)
+    for s in range(args.warmup + steps):
+        rows = (np.arange(n) * max(1, B_total // n) + s) % B_total
+        Y = make_signals(A_np, rows, cfg["seed"], cfg["sparsity"], cfg["sigma"])
+        t0 = time.perf_counter()
+        oracle_batch(A_np, Y, cfg["S"], eps32, workers=cores)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = statistics.mean(times) * 1e3
+    value = n / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg['name']}: M={cfg['M']} N={cfg['N']} S={cfg['S']} B={B_total}",
+                   "global_batch": B_total, "step_sample": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
+                         "sample": f"{n} signals per step of {cfg['name']}, FP64 numpy QR per OMP step, "
+                                   f"one process per core"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

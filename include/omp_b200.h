@@ -67,16 +67,19 @@ typedef enum {
   OMP_SIG_NAN = 3          /* y_b (hence a correlation) is not finite                        */
 } ompSigStatus_t;
 
-/* how the correlation C = A^T R is contracted */
+/* how the correlation C = A^T R is evaluated.  In both tensor-core modes the
+ * tcgen05 GEMM is a screen with a rigorous error bound; every atom inside the bound window is then
+ * re-evaluated as an exact FP32 dot, so the selected atom is the FP32 argmax. */
 typedef enum {
-  OMP_CORR_3XTF32 = 0,     /* tcgen05 tensor cores, C = Ahi'Rhi + Ahi'Rlo + Alo'Rhi (FP32-accurate) */
-  OMP_CORR_FP32_SIMT = 1   /* FP32 FFMA tiled GEMM (fallback / cross-check)                         */
+  OMP_CORR_BF16 = 0,        /* default: bf16 tcgen05 screen (kind::f16) + FP32 re-evaluation          */
+  OMP_CORR_FP32_SIMT = 1,   /* FP32 FFMA GEMM writes C; standalone argmax kernel (fallback)           */
+  OMP_CORR_3XTF32 = 2       /* 3xTF32 tcgen05 screen (kind::tf32, tighter window) + FP32 re-evaluation */
 } ompCorrMode_t;
 
 /* ompCreate — bind a dictionary to `device` and run the one-time setup (K0):
  *   validate A (finite, every ||a_n|| > 0), ||a_n|| in FP64 and 1/||a_n||,
- *   TF32 hi/lo planes of A^T, and the Gram matrix G = A^T A by the
- *   same correlation kernel.  Setup cost is amortised across batches.
+ *   the screening planes of A^T, and the Gram matrix G = A^T A in FP32.
+ *   Setup cost is amortised across batches.
  *   A: device, M x N column-major, lda >= M.  Synchronises `stream` before returning.
  *   Errors: OMP_ERR_INVALID_ARG (M,N < 1, lda < M, A == NULL, bad mode),
  *           OMP_ERR_ZERO_COLUMN / OMP_ERR_NONFINITE (no handle is returned),
@@ -113,8 +116,9 @@ ompStatus_t ompDensify(ompHandle_t handle, const float* X, int64_t ldx, const in
                        int64_t lds, const int32_t* n_iter, int64_t B, int32_t S, float* Xdense,
                        int64_t ldxd, void* stream);
 
-/* ompCorrelate — the correlation step alone: C[b*ldc + n] = sum_m R[b*ldr + m] A[m, n]
- *   ("a single call to gemm"), through the handle's correlation kernel.
+/* ompCorrelate — the correlation GEMM alone: C[b*ldc + n] = sum_m R[b*ldr + m] A[m, n]
+ *   ("a single call to gemm"), through the handle's correlation kernel
+ *   (tensor-core modes return the SCREEN values, accurate to the mode's bound c0 ||a|| ||r||).
  *   R: B x M row-major (= M x B column-major), ldr >= M.  C: B x N row-major, ldc >= N.
  *   Diagnostic / test entry point.                                                         */
 ompStatus_t ompCorrelate(ompHandle_t handle, const float* R, int64_t B, int64_t ldr, float* C,

@@ -28,8 +28,9 @@ OMP_SIG_EPS = 1
 OMP_SIG_DEGENERATE = 2
 OMP_SIG_NAN = 3
 
-OMP_CORR_3XTF32 = 0
+OMP_CORR_BF16 = 0
 OMP_CORR_FP32_SIMT = 1
+OMP_CORR_3XTF32 = 2
 OMP_NUM_KERNEL_SLOTS = 5
 KERNEL_SLOTS = ("init", "correlation", "select", "factor_append", "residual")
 

@@ -1,7 +1,8 @@
 // K1-SIMT: the correlation C = A^T R ("a single call to gemm") as an FP32
 // FFMA tiled GEMM.  Fallback / cross-check for the tcgen05 path (BASELINE.json north_star
-// "with FP32 SIMT as fallback").  Operands are the TF32 hi/lo planes; hi + lo reproduces
-// the FP32 value exactly, so this is a plain FP32 GEMM on the original data.
+// "with FP32 SIMT as fallback").  Plain FP32 on the fp32 planes: round-to-nearest FFMA,
+// sequential over K, so its error does not drift with K like the truncating tensor-core
+// accumulator does.
 //   C[b, n] = sum_k R[b, k] * At[n, k]   (both K-major)
 // Tile 128 (signals) x 128 (atoms) x 16, 256 threads, 8 x 8 outputs per thread.
 #include "omp_internal.cuh"
@@ -10,10 +11,9 @@ namespace ompb {
 
 constexpr int SB = 128, SN = 128, SK = 16, SPAD = 4;
 
-__global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rh, const float* __restrict__ Rl,
-                                                    int64_t ldr, int64_t B, const float* __restrict__ Ah,
-                                                    const float* __restrict__ Al, int64_t lda, int64_t NA,
-                                                    int64_t K, float* __restrict__ C, int64_t ldc) {
+__global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rm, int64_t ldr, int64_t B,
+                                                    const float* __restrict__ Am, int64_t lda, int64_t NA,
+                                                    int64_t K, float* __restrict__ C, int64_t ldc, int64_t ncols) {
   __shared__ float As[SK][SB + SPAD];   // R tile, transposed: As[k][row]
   __shared__ float Bs[SK][SN + SPAD];   // At tile, transposed: Bs[k][atom]
   const int tid = threadIdx.x;
@@ -31,21 +31,13 @@ __global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rh
       const int idx = tid + h * 256;       // 512 float4 per operand tile
       const int row = idx >> 2, kq = idx & 3;
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (b0 + row < B) {
-        const float4 a = *reinterpret_cast<const float4*>(Rh + (b0 + row) * ldr + k0 + kq * 4);
-        const float4 c = *reinterpret_cast<const float4*>(Rl + (b0 + row) * ldr + k0 + kq * 4);
-        r = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
-      }
+      if (b0 + row < B) r = *reinterpret_cast<const float4*>(Rm + (b0 + row) * ldr + k0 + kq * 4);
       As[kq * 4 + 0][row] = r.x;
       As[kq * 4 + 1][row] = r.y;
       As[kq * 4 + 2][row] = r.z;
       As[kq * 4 + 3][row] = r.w;
       float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (n0 + row < NA) {
-        const float4 a = *reinterpret_cast<const float4*>(Ah + (n0 + row) * lda + k0 + kq * 4);
-        const float4 c = *reinterpret_cast<const float4*>(Al + (n0 + row) * lda + k0 + kq * 4);
-        t = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
-      }
+      if (n0 + row < NA) t = *reinterpret_cast<const float4*>(Am + (n0 + row) * lda + k0 + kq * 4);
       Bs[kq * 4 + 0][row] = t.x;
       Bs[kq * 4 + 1][row] = t.y;
       Bs[kq * 4 + 2][row] = t.z;
@@ -77,18 +69,20 @@ __global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rh
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t col = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      if (col < NA) C[row * ldc + col] = acc[i][j];
+      if (col < ncols) C[row * ldc + col] = acc[i][j];
     }
   }
 }
 
-cudaError_t launch_corr_simt(const Planes& R, const Planes& At, int64_t K, float* C, int64_t ldc,
-                             cudaStream_t st) {
+cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
+                             int64_t ncols, cudaStream_t st) {
   if (R.rows == 0) return cudaSuccess;
   if (K % SK != 0 || R.ld % 4 != 0 || At.ld % 4 != 0) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)((At.rows + SN - 1) / SN), (unsigned)((R.rows + SB - 1) / SB));
+  if (ncols > At.rows) ncols = At.rows;
+  dim3 grid((unsigned)((ncols + SN - 1) / SN), (unsigned)((R.rows + SB - 1) / SB));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k1_corr_simt<<<grid, 256, 0, st>>>(R.hi, R.lo, R.ld, R.rows, At.hi, At.lo, At.ld, At.rows, K, C, ldc);
+  k1_corr_simt<<<grid, 256, 0, st>>>((const float*)R.plane[0], R.ld, R.rows, (const float*)At.plane[0], At.ld,
+                                     At.rows, K, C, ldc, ncols);
   return cudaGetLastError();
 }
 

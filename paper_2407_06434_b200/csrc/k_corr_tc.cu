@@ -1,8 +1,513 @@
-// K1 tensor-core path (tcgen05 / TMA / TMEM, 3xTF32) — placeholder until the kernel lands.
+// K1: the correlation C = A^T R as ONE batched GEMM (PAPER.md:204-212,
+// "a single call to gemm") on the 5th-generation tensor cores, used as a SCREEN:
+//   KIND_BF16  : C~ = bf16(A)' bf16(R)                       (kind::f16, 1 MMA per K step)
+//   KIND_3XTF32: C~ = Ahi'Rhi + Ahi'Rlo + Alo'Rhi            (kind::tf32, 3 MMAs per K step)
+// Measured on B200 (scripts/diag_accum.py): the tensor-core FP32 accumulator
+// truncates, so even 3xTF32 drifts by ~1e-5 relative at K = 2048 — above the 1e-5 near-tie
+// budget.  The kernel therefore does not decide the argmax; its epilogue emits, per signal and
+// 256-atom tile, the top-4 candidates of |c~_n| / ||a_n||, and the refine kernel (k_refine.cu)
+// re-evaluates every atom inside the rigorous error window c0 ||r|| in exact FP32.
+// Blackwell-native structure:
+//   * operands staged by TMA (cp.async.bulk.tensor, 128-byte swizzle) into an mbarrier ring;
+//   * one elected thread issues tcgen05.mma into TMEM accumulators (UMMA M = 128 signals per
+//     CTA, N = 256 atoms); two accumulators (2 x 256 of the 512 TMEM columns) so the epilogue of
+//     tile i overlaps the MMAs of tile i+1; tcgen05.commit -> mbarrier hand-offs only;
+//   * persistent grid (one CTA / CTA pair per SM), static tile schedule rasterised in groups of
+//     GM row-blocks so concurrently running tiles share A and R slabs in L2;
+//   * CG = 2: cta_group::2 pairs two SMs on a 256 x 256 tile (each CTA stages its 128 signal
+//     rows and half of the atoms; the leader issues the MMA), halving per-SM operand traffic.
+// Epilogues: MODE_STORE writes C~ (ompCorrelate, numerics tests); MODE_TOPK writes partials.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "omp_internal.cuh"
 
 namespace ompb {
-cudaError_t launch_corr_tc(const Planes&, const Planes&, int64_t, float*, int64_t, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace tc {
+
+constexpr int BM = 128;       // signal rows per CTA (UMMA M per CTA)
+constexpr int BN = 256;       // atoms per tile (UMMA N)
+constexpr int GM = 16;        // row-blocks per raster group
+constexpr int NUM_THREADS = 256;
+constexpr int MODE_STORE = 0, MODE_TOPK = 1;
+
+// Operand kinds.  Every stage holds one 128-byte-wide K slab of each plane.
+template <int KIND>
+struct Kind;
+template <>
+struct Kind<KIND_BF16> {
+  static constexpr int ELEM = 2, BK = 64, UK = 16, NPLANES = 1;
+  static constexpr uint32_t FMT = 1;   // BF16
+};
+template <>
+struct Kind<KIND_3XTF32> {
+  static constexpr int ELEM = 4, BK = 32, UK = 8, NPLANES = 2;   // hi, lo
+  static constexpr uint32_t FMT = 2;   // TF32
+};
+
+template <int KIND, int CG>
+struct Cfg {
+  using K_ = Kind<KIND>;
+  static constexpr int BN_CTA = BN / CG;
+  static constexpr uint32_t R_BYTES = BM * K_::BK * K_::ELEM;        // one plane of the R tile
+  static constexpr uint32_t A_BYTES = BN_CTA * K_::BK * K_::ELEM;    // one plane of the A tile
+  static constexpr uint32_t STAGE_BYTES = K_::NPLANES * (R_BYTES + A_BYTES);
+  static constexpr int STAGES = (int)((200u * 1024u) / STAGE_BYTES) < 8 ? (int)((200u * 1024u) / STAGE_BYTES) : 8;
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC = (1u << 4)                            // D = F32
+                                    | (K_::FMT << 7) | (K_::FMT << 10)   // A, B formats
+                                    | ((uint32_t)(BN >> 3) << 17)        // N
+                                    | ((uint32_t)((BM * CG) >> 4) << 24);  // M
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+// arrive on the barrier at the same offset in CTA rank 0 of the cluster (own CTA when CG = 1)
+__device__ __forceinline__ void mbar_arrive_cta0(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu)
+               : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int k, int row) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+  }
+}
+
+// K-major, 128-byte-swizzled UMMA shared-memory descriptor (8-row x 128 B atoms, SBO = 1024 B)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+template <int KIND, int CG>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+#define OMPB_MMA(KINDSTR, CGSTR)                                                   \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                   \
+               "tcgen05.mma.cta_group::" CGSTR ".kind::" KINDSTR " [%0], %1, %2, %3, p;\n\t}" \
+               ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory")
+  if constexpr (KIND == KIND_BF16) {
+    if constexpr (CG == 1) OMPB_MMA("f16", "1"); else OMPB_MMA("f16", "2");
+  } else {
+    if constexpr (CG == 1) OMPB_MMA("tf32", "1"); else OMPB_MMA("tf32", "2");
+  }
+#undef OMPB_MMA
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+  } else {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+  }
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+struct TileSched {
+  int tiles_m, tiles_n;
+  __device__ void coords(int t, int& tm, int& tn) const {
+    const int per_group = GM * tiles_n;
+    const int g = t / per_group;
+    const int first = g * GM;
+    const int gm = min(GM, tiles_m - first);
+    const int local = t - g * per_group;
+    tm = first + local % gm;
+    tn = local / gm;
+  }
+};
+
+struct EpiArgs {
+  float* C;                 // MODE_STORE
+  int64_t ldc;
+  int64_t ncols;            // columns < ncols are stored
+  const float* inv_norm;    // MODE_TOPK
+  float2* part;             // MODE_TOPK: rows x tiles_n x TOPK {value, index bits}
+  const int32_t* status;    // MODE_TOPK: finished rows are skipped (may be null)
+};
+
+struct Maps {
+  CUtensorMap r[2];         // R planes (bf16: r[0]; 3xtf32: hi, lo)
+  CUtensorMap a[2];         // A^T planes
+};
+
+template <int KIND, int CG, int MODE>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m, int tiles_n, EpiArgs ep) {
+  using C_ = Cfg<KIND, CG>;
+  using K_ = Kind<KIND>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::STAGES * C_::STAGE_BYTES);
+  uint64_t* empty = full + C_::STAGES;
+  uint64_t* tfull = empty + C_::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
+  const int num_tiles = tiles_m * tiles_n;
+  const TileSched sched{tiles_m, tiles_n};
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C_::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128 * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (one thread per CTA) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int tm, tn;
+        sched.coords(t, tm, tn);
+        const int row0 = tm * BM * CG + (int)rank * BM;
+        const int atom0 = tn * BN + (int)rank * C_::BN_CTA;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C_::STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[stage], C_::STAGE_BYTES * CG);
+#pragma unroll
+          for (int p = 0; p < K_::NPLANES; ++p) {
+            tma_load_2d<CG>(&maps.r[p], &full[stage], st + p * C_::R_BYTES, kb * K_::BK, row0);
+            tma_load_2d<CG>(&maps.a[p], &full[stage], st + K_::NPLANES * C_::R_BYTES + p * C_::A_BYTES,
+                            kb * K_::BK, atom0);
+          }
+          if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+        const int a = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[a], aphase ^ 1);
+        fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(a * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t base = smem_u32(smem + stage * C_::STAGE_BYTES);
+          const uint64_t dr0 = desc_sw128(base);
+          const uint64_t da0 = desc_sw128(base + K_::NPLANES * C_::R_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < K_::BK / K_::UK; ++kk) {
+            const uint64_t off = (uint64_t)((kk * K_::UK * K_::ELEM) >> 4);   // +32 B per K step
+            if constexpr (KIND == KIND_BF16) {
+              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb | kk) != 0);
+            } else {
+              const uint64_t dr1 = desc_sw128(base + C_::R_BYTES);
+              const uint64_t da1 = desc_sw128(base + 2 * C_::R_BYTES + C_::A_BYTES);
+              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb | kk) != 0);   // Rhi Ahi
+              mma<KIND, CG>(d, dr1 + off, da0 + off, C_::IDESC, 1u);                // Rlo Ahi
+              mma<KIND, CG>(d, dr0 + off, da1 + off, C_::IDESC, 1u);                // Rhi Alo
+            }
+          }
+          mma_commit<CG>(&empty[stage]);          // slot free once these MMAs have read it
+          if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit<CG>(&tfull[a]);                // accumulator a complete
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> registers -> global =====================
+    const int ew = warp - 4;
+    int it = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+      int tm, tn;
+      sched.coords(t, tm, tn);
+      const int a = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[a], aphase);
+      fence_after();
+      const int row = tm * BM * CG + (int)rank * BM + ew * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(a * BN);
+      bool live = row < rows;
+      if constexpr (MODE == MODE_TOPK) {
+        if (live && ep.status) live = ep.status[row] == SIG_RUNNING;
+      }
+      float bv[TOPK];
+      int bi[TOPK];
+#pragma unroll
+      for (int j = 0; j < TOPK; ++j) { bv[j] = -1.f; bi[j] = -1; }
+      bool nan_seen = false;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + (uint32_t)(c * 32), v);
+        const int64_t col0 = (int64_t)tn * BN + c * 32;
+        if constexpr (MODE == MODE_STORE) {
+          if (live) {
+            float* dst = ep.C + (int64_t)row * ep.ldc + col0;
+            if (col0 + 32 <= ep.ncols && (ep.ldc & 3) == 0) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (col0 + q < ep.ncols) dst[q] = v[q];
+            }
+          }
+        } else {
+          if (live) {
+            const float4* w4 = reinterpret_cast<const float4*>(ep.inv_norm + col0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 w = __ldg(w4 + q);
+              const float wq[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float x = v[4 * q + e];
+                nan_seen |= isnan(x);
+                const float s = fabsf(x) * wq[e];
+                if (s > bv[TOPK - 1]) {        // insert, keeping equal values in index order
+                  float cv = s;
+                  int ci = (int)col0 + 4 * q + e;
+#pragma unroll
+                  for (int j = 0; j < TOPK; ++j) {
+                    if (cv > bv[j]) {
+                      const float tv = bv[j];
+                      const int ti = bi[j];
+                      bv[j] = cv; bi[j] = ci;
+                      cv = tv; ci = ti;
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+      if constexpr (MODE == MODE_TOPK) {
+        if (live) {
+          if (nan_seen) bi[0] = SEL_NAN;
+          float4* dst = reinterpret_cast<float4*>(ep.part + ((int64_t)row * tiles_n + tn) * TOPK);
+#pragma unroll
+          for (int j = 0; j < TOPK; j += 2)
+            dst[j / 2] = make_float4(bv[j], __int_as_float(bi[j]), bv[j + 1], __int_as_float(bi[j + 1]));
+        }
+      }
+      fence_before();
+      mbar_arrive_cta0(&tempty[a]);
+    }
+  }
+
+  // teardown (reconverge the single-lane role loops before the aligned barriers)
+  __syncwarp();
+  fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  fence_after();
+  if (warp == 2) {
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <int KIND>
+static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ld_elems, int64_t K, int box_rows) {
+  using K_ = Kind<KIND>;
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * K_::ELEM)};
+  cuuint32_t box[2] = {(cuuint32_t)K_::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = KIND == KIND_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return f(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+template <int KIND, int CG, int MODE>
+static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const EpiArgs& ep, cudaStream_t st) {
+  using C_ = Cfg<KIND, CG>;
+  using K_ = Kind<KIND>;
+  if (R.rows == 0) return cudaSuccess;
+  if (K % K_::BK != 0 || At.rows % BN != 0 || R.rows > INT32_MAX) return cudaErrorNotSupported;
+  Maps maps;
+  for (int p = 0; p < K_::NPLANES; ++p) {
+    if (!make_map<KIND>(&maps.r[p], R.plane[p], R.rows, R.ld, K, BM) ||
+        !make_map<KIND>(&maps.a[p], At.plane[p], At.rows, At.ld, K, C_::BN_CTA))
+      return cudaErrorNotSupported;
+  }
+  if (K_::NPLANES == 1) {
+    maps.r[1] = maps.r[0];
+    maps.a[1] = maps.a[0];
+  }
+  auto kern = k1_corr_tc<KIND, CG, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = (int)((R.rows + BM * CG - 1) / (BM * CG));
+  const int tiles_n = (int)(At.rows / BN);
+  const int tiles = tiles_m * tiles_n;
+  const int max_clusters = num_sms() / CG;
+  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C_::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps, (int)R.rows, (int)(K / K_::BK), tiles_m, tiles_n, ep);
+}
+
+template <int MODE>
+static cudaError_t dispatch(int kind, const Operand& R, const Operand& At, int64_t K, const EpiArgs& ep,
+                           cudaStream_t st) {
+  static int cg = 0;
+  if (!cg) {
+    const char* env = getenv("OMP_B200_CTA_GROUP");
+    cg = (env && env[0] == '1') ? 1 : 2;
+  }
+  if (kind == KIND_BF16)
+    return cg == 1 ? launch<KIND_BF16, 1, MODE>(R, At, K, ep, st) : launch<KIND_BF16, 2, MODE>(R, At, K, ep, st);
+  if (kind == KIND_3XTF32)
+    return cg == 1 ? launch<KIND_3XTF32, 1, MODE>(R, At, K, ep, st) : launch<KIND_3XTF32, 2, MODE>(R, At, K, ep, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tc
+
+cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
+                           int64_t ncols, cudaStream_t st) {
+  tc::EpiArgs ep{C, ldc, ncols, nullptr, nullptr, nullptr};
+  return tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
+}
+
+cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const float* inv_norm,
+                                const int32_t* status, float2* part, cudaStream_t st) {
+  tc::EpiArgs ep{nullptr, 0, At.rows, inv_norm, part, status};
+  return tc::dispatch<tc::MODE_TOPK>(kind, R, At, K, ep, st);
+}
+
 }  // namespace ompb

@@ -19,7 +19,8 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k2_select(const float* __restrict__ C, int64_t ldc, int64_t N,
                                                      const float* __restrict__ inv_norm,
                                                      const int32_t* __restrict__ status,
-                                                     int32_t* __restrict__ nstar, bool vec) {
+                                                     int32_t* __restrict__ nstar, float* __restrict__ cstar,
+                                                     bool vec) {
   const int64_t b = blockIdx.x;
   if (status[b] != SIG_RUNNING) return;
   const float* c = C + b * ldc;
@@ -71,18 +72,19 @@ __global__ void __launch_bounds__(THREADS) k2_select(const float* __restrict__ C
 #pragma unroll
     for (int w = 1; w < THREADS / 32; ++w) r = better(r, red[w]);
     nstar[b] = any_nan ? SEL_NAN : (r.v > 0.f ? r.i : SEL_DEGENERATE);
+    cstar[b] = (!any_nan && r.v > 0.f) ? c[r.i] : 0.f;   // signed <r, a_{n*}>
   }
 }
 
 cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, const float* inv_norm,
-                          const int32_t* status, int32_t* nstar, cudaStream_t st) {
+                          const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(inv_norm) & 15) == 0);
   if (N >= 2048)
-    k2_select<256><<<(unsigned)B, 256, 0, st>>>(C, ldc, N, inv_norm, status, nstar, vec);
+    k2_select<256><<<(unsigned)B, 256, 0, st>>>(C, ldc, N, inv_norm, status, nstar, cstar, vec);
   else
-    k2_select<128><<<(unsigned)B, 128, 0, st>>>(C, ldc, N, inv_norm, status, nstar, vec);
+    k2_select<128><<<(unsigned)B, 128, 0, st>>>(C, ldc, N, inv_norm, status, nstar, cstar, vec);
   return cudaGetLastError();
 }
 

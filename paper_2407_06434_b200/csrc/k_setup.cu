@@ -1,8 +1,10 @@
-// K0 (dictionary setup), batch init (a1), densify (a6) and the TF32 hi/lo split.
+// K0 (dictionary setup), batch init (a1), densify (a6) and the operand planes of K1.
 //
-// TF32 split (3xTF32): hi = rna_tf32(x) keeps the 11 leading
-// significand bits, lo = x - hi is exact in FP32, so hi + lo == x bit for bit and the
-// tensor-core products Ahi'Rhi + Ahi'Rlo + Alo'Rhi reproduce an FP32-accurate dot.
+// Planes written for every row (atom of A^T, or residual of a signal), padded to Mp with zeros:
+//   fp32 copy           (gather in K4, exact re-evaluation in the refine kernel, SIMT GEMM)
+//   bf16  = RN(x)       (BF16 tcgen05 screen)
+//   tf32 hi = RNA(x), lo = x - hi (exact in FP32)   (3xTF32 tcgen05 screen)
+#include <cuda_bf16.h>
 #include <math.h>
 
 #include "omp_internal.cuh"
@@ -13,6 +15,18 @@ __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void put_planes(int64_t off, float v, float* __restrict__ P32,
+                                           __nv_bfloat16* __restrict__ Pb, float* __restrict__ Phi,
+                                           float* __restrict__ Plo) {
+  if (P32) P32[off] = v;
+  if (Pb) Pb[off] = __float2bfloat16_rn(v);
+  if (Phi) {
+    const float h = tf32_rna(v);
+    Phi[off] = h;
+    Plo[off] = v - h;
+  }
 }
 
 __device__ __forceinline__ double block_sum_double(double v, double* red) {
@@ -29,12 +43,12 @@ __device__ __forceinline__ double block_sum_double(double v, double* red) {
   return red[0];
 }
 
-// One CTA per (padded) atom n: copy a_n into row n of At (Np x Mp, zero padded), split it,
-// and compute ||a_n|| in FP64 (PAPER.md:46 denominator; App. A).
-__global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t N, int64_t lda,
-                                 int64_t Mp, float* __restrict__ At, float* __restrict__ At_hi,
-                                 float* __restrict__ At_lo, float* __restrict__ inv_norm,
-                                 int* bad_zero, int* bad_nonfinite) {
+// One CTA per (padded) atom n: copy a_n into row n of the planes and compute ||a_n|| in FP64
+// (PAPER.md:46 denominator; App. A).
+__global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t N, int64_t lda, int64_t Mp,
+                                 float* __restrict__ At, __nv_bfloat16* __restrict__ Ab, float* __restrict__ Ahi,
+                                 float* __restrict__ Alo, float* __restrict__ inv_norm, int* bad_zero,
+                                 int* bad_nonfinite) {
   __shared__ double red[32];
   const int64_t n = blockIdx.x;
   double ss = 0.0;
@@ -46,10 +60,7 @@ __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t
       finite &= isfinite(v);
       ss += (double)v * (double)v;
     }
-    const float h = tf32_rna(v);
-    At[n * Mp + m] = v;
-    At_hi[n * Mp + m] = h;
-    At_lo[n * Mp + m] = v - h;
+    put_planes(n * Mp + m, v, At, Ab, Ahi, Alo);
   }
   const int any_bad = __syncthreads_or(!finite);
   ss = block_sum_double(ss, red);
@@ -64,39 +75,36 @@ __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t
   }
 }
 
-cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp,
-                                 int64_t Np, float* At, float* At_hi, float* At_lo, float* inv_norm,
+cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
+                                 float* At, void* At_bf16, float* At_hi, float* At_lo, float* inv_norm,
                                  int* bad_zero, int* bad_nonfinite, cudaStream_t st) {
-  k0_prepare_atoms<<<(unsigned)Np, 128, 0, st>>>(A, M, N, lda, Mp, At, At_hi, At_lo, inv_norm,
-                                                 bad_zero, bad_nonfinite);
+  k0_prepare_atoms<<<(unsigned)Np, 128, 0, st>>>(A, M, N, lda, Mp, At, (__nv_bfloat16*)At_bf16, At_hi, At_lo,
+                                                 inv_norm, bad_zero, bad_nonfinite);
   return cudaGetLastError();
 }
 
-__global__ void k_split_rows(const float* __restrict__ R, int64_t ldr, int64_t M, int64_t Mp,
-                             float* __restrict__ R_hi, float* __restrict__ R_lo) {
+__global__ void k_make_planes(const float* __restrict__ R, int64_t ldr, int64_t M, int64_t Mp,
+                              float* __restrict__ R32, __nv_bfloat16* __restrict__ Rb, float* __restrict__ Rhi,
+                              float* __restrict__ Rlo) {
   const int64_t b = blockIdx.x;
-  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
-    const float v = m < M ? R[b * ldr + m] : 0.f;
-    const float h = tf32_rna(v);
-    R_hi[b * Mp + m] = h;
-    R_lo[b * Mp + m] = v - h;
-  }
+  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x)
+    put_planes(b * Mp + m, m < M ? R[b * ldr + m] : 0.f, R32, Rb, Rhi, Rlo);
 }
 
-cudaError_t launch_split_rows(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp,
-                              float* R_hi, float* R_lo, cudaStream_t st) {
+cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp, float* R32,
+                               void* Rb, float* R_hi, float* R_lo, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  k_split_rows<<<(unsigned)B, 128, 0, st>>>(R, ldr, M, Mp, R_hi, R_lo);
+  k_make_planes<<<(unsigned)B, 128, 0, st>>>(R, ldr, M, Mp, R32, (__nv_bfloat16*)Rb, R_hi, R_lo);
   return cudaGetLastError();
 }
 
 // a1: x_0 = 0, r_0 = y; eps is tested on r_0 (reading R2);
 // support = -1, n_iter = 0.  One CTA per signal.
-__global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M, int64_t Mp,
-                             int32_t S, float eps, float* __restrict__ R_hi, float* __restrict__ R_lo,
-                             float* __restrict__ X, int64_t ldx, int32_t* __restrict__ support,
-                             int64_t lds, float* __restrict__ resid, int32_t* __restrict__ n_iter,
-                             int32_t* __restrict__ status) {
+__global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M, int64_t Mp, int32_t S, float eps,
+                             float* __restrict__ R32, __nv_bfloat16* __restrict__ Rb, float* __restrict__ Rhi,
+                             float* __restrict__ Rlo, float* __restrict__ X, int64_t ldx,
+                             int32_t* __restrict__ support, int64_t lds, float* __restrict__ resid,
+                             int32_t* __restrict__ n_iter, int32_t* __restrict__ status) {
   __shared__ double red[32];
   const int64_t b = blockIdx.x;
   const float* y = Y + b * ldy;
@@ -104,9 +112,7 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
   for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
     const float v = m < M ? y[m] : 0.f;
     part = fmaf(v, v, part);
-    const float h = tf32_rna(v);
-    R_hi[b * Mp + m] = h;
-    R_lo[b * Mp + m] = v - h;
+    put_planes(b * Mp + m, v, R32, Rb, Rhi, Rlo);
   }
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     X[b * ldx + j] = 0.f;
@@ -126,13 +132,13 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
   }
 }
 
-cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp,
-                              int32_t S, float eps, float* R_hi, float* R_lo, float* X, int64_t ldx,
-                              int32_t* support, int64_t lds, float* resid, int32_t* n_iter,
-                              int32_t* status, cudaStream_t st) {
+cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
+                              float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
+                              int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
+                              cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  k_batch_init<<<(unsigned)B, 128, 0, st>>>(Y, ldy, M, Mp, S, eps, R_hi, R_lo, X, ldx, support,
-                                            lds, resid, n_iter, status);
+  k_batch_init<<<(unsigned)B, 128, 0, st>>>(Y, ldy, M, Mp, S, eps, R32, (__nv_bfloat16*)Rb, R_hi, R_lo, X, ldx,
+                                            support, lds, resid, n_iter, status);
   return cudaGetLastError();
 }
 

@@ -5,12 +5,14 @@
 //   w = A_k^T a_{n*} = [A^T A]_{n*, S_k}    (Gram entries)
 //   z = F_k^T w,  gamma = 1/sqrt(||a_{n*}||^2 - ||z||^2)
 //   F_{k+1} = [[F_k, -gamma F_k z], [0, gamma]]                               (Eq. 8)
-//   u = F^T A^T y grows by u_new = gamma (a_{n*}^T y - z^T u)   (Eq. 2 append)
+//   u = F^T A^T y grows by u_new = f^T A_{k+1}^T y = gamma a_{n*}^T r_k = gamma c*
+//     (the new basis vector q = A_{k+1} f is orthogonal to span A_k, so q^T y = q^T r_k; pin P9)
 //   x = F_{k+1} u  (matrix-vector products only, Eq. 11)
 // F is upper triangular and packed by columns (column j = F[0..j, j] at offset j(j+1)/2),
 // the paper's packed representation applied to the factor, so the
 // leading block is a contiguous prefix and appending a column is a contiguous write.
 // Every live signal is at the same k (= iteration), so k is a kernel argument.
+#include <cuda_bf16.h>
 #include <math.h>
 
 #include "omp_internal.cuh"
@@ -38,8 +40,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 template <int T>
 __global__ void __launch_bounds__(T) k3_factor_append(
-    int32_t k, const int32_t* __restrict__ nstar, const float* __restrict__ G, int64_t ldg,
-    const float* __restrict__ P0, int64_t ldp, float* __restrict__ F, int64_t ldf,
+    int32_t k, const int32_t* __restrict__ nstar, const float* __restrict__ cstar, const float* __restrict__ G,
+    int64_t ldg, float* __restrict__ F, int64_t ldf,
     float* __restrict__ U, int64_t ldu, float* __restrict__ X, int64_t ldx,
     int32_t* __restrict__ support, int64_t lds, int32_t* __restrict__ status) {
   const int64_t b = blockIdx.x;
@@ -75,13 +77,9 @@ __global__ void __launch_bounds__(T) k3_factor_append(
     if (lane == 0) z[j] = acc;
   }
   __syncthreads();
-  float zz = 0.f, zu = 0.f;
-  for (int j = threadIdx.x; j < k; j += T) {
-    zz = fmaf(z[j], z[j], zz);
-    zu = fmaf(z[j], u[j], zu);
-  }
+  float zz = 0.f;
+  for (int j = threadIdx.x; j < k; j += T) zz = fmaf(z[j], z[j], zz);
   zz = block_sum<T>(zz, red);
-  zu = block_sum<T>(zu, red);
   const float d = grow[n];              // ||a_{n*}||^2
   const float delta = d - zz;
   if (!(delta > TAU_F * d)) {           // rank deficiency (reading R6); also catches NaN
@@ -89,8 +87,7 @@ __global__ void __launch_bounds__(T) k3_factor_append(
     return;
   }
   const float gamma = 1.0f / sqrtf(delta);
-  const float beta = P0[b * ldp + n];   // a_{n*}^T y
-  const float unew = gamma * (beta - zu);
+  const float unew = gamma * cstar[b];  // gamma <r_k, a_{n*}>
   // v = F_k z and t = F_k u in one pass over F (thread per row, coalesced per column)
   float* newcol = Fb + (int64_t)k * (k + 1) / 2;
   for (int i = threadIdx.x; i < k; i += T) {
@@ -112,13 +109,12 @@ __global__ void __launch_bounds__(T) k3_factor_append(
   }
 }
 
-cudaError_t launch_factor_append(int32_t k, int64_t B, const int32_t* nstar, const float* G,
-                                 int64_t ldg, const float* P0, int64_t ldp, float* F, int64_t ldf,
-                                 float* u, int64_t ldu, float* X, int64_t ldx, int32_t* support,
-                                 int64_t lds, int32_t* status, cudaStream_t st) {
+cudaError_t launch_factor_append(int32_t k, int64_t B, const int32_t* nstar, const float* cstar, const float* G,
+                                 int64_t ldg, float* F, int64_t ldf, float* u, int64_t ldu, float* X, int64_t ldx,
+                                 int32_t* support, int64_t lds, int32_t* status, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  k3_factor_append<128><<<(unsigned)B, 128, 0, st>>>(k, nstar, G, ldg, P0, ldp, F, ldf, u, ldu, X,
-                                                     ldx, support, lds, status);
+  k3_factor_append<128><<<(unsigned)B, 128, 0, st>>>(k, nstar, cstar, G, ldg, F, ldf, u, ldu, X, ldx, support, lds,
+                                                     status);
   return cudaGetLastError();
 }
 
@@ -131,8 +127,8 @@ template <int T, int CH>
 __global__ void __launch_bounds__(T) k4_residual(
     int32_t k, int32_t S, float eps, const float* __restrict__ Y, int64_t ldy, int64_t M, int64_t Mp,
     const float* __restrict__ At, const float* __restrict__ X, int64_t ldx,
-    const int32_t* __restrict__ support, int64_t lds, float* __restrict__ R_hi,
-    float* __restrict__ R_lo, float* __restrict__ resid, int32_t* __restrict__ n_iter,
+    const int32_t* __restrict__ support, int64_t lds, float* __restrict__ R32, __nv_bfloat16* __restrict__ Rb,
+    float* __restrict__ R_hi, float* __restrict__ R_lo, float* __restrict__ resid, int32_t* __restrict__ n_iter,
     int32_t* __restrict__ status, bool yvec) {
   const int64_t b = blockIdx.x;
   if (status[b] != SIG_RUNNING) return;
@@ -168,8 +164,7 @@ __global__ void __launch_bounds__(T) k4_residual(
   }
   const float* y = Y + b * ldy;
   float part = 0.f;
-  float4* Rh = reinterpret_cast<float4*>(R_hi + b * Mp);
-  float4* Rl = reinterpret_cast<float4*>(R_lo + b * Mp);
+  float4* R4 = reinterpret_cast<float4*>(R32 + b * Mp);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int64_t q = threadIdx.x + (int64_t)c * T;
@@ -186,9 +181,19 @@ __global__ void __launch_bounds__(T) k4_residual(
       }
       float4 r = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
       part = fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, fmaf(r.w, r.w, part))));
-      float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
-      Rh[q] = h;
-      Rl[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
+      R4[q] = r;
+      if (Rb) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&p0);
+        pk.y = *reinterpret_cast<uint32_t*>(&p1);
+        reinterpret_cast<uint2*>(Rb + b * Mp)[q] = pk;
+      }
+      if (R_hi) {
+        const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
+        reinterpret_cast<float4*>(R_hi + b * Mp)[q] = h;
+        reinterpret_cast<float4*>(R_lo + b * Mp)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
+      }
     }
   }
   const float rr = block_sum<T>(part, red);
@@ -204,31 +209,31 @@ __global__ void __launch_bounds__(T) k4_residual(
 template <int T, int CH>
 static void launch_k4(int32_t k, int32_t S, float eps, int64_t B, const float* Y, int64_t ldy, int64_t M,
                       int64_t Mp, const float* At, const float* X, int64_t ldx, const int32_t* support,
-                      int64_t lds, float* R_hi, float* R_lo, float* resid, int32_t* n_iter,
+                      int64_t lds, float* R32, void* Rb, float* R_hi, float* R_lo, float* resid, int32_t* n_iter,
                       int32_t* status, bool yvec, cudaStream_t st) {
-  k4_residual<T, CH><<<(unsigned)B, T, 0, st>>>(k, S, eps, Y, ldy, M, Mp, At, X, ldx, support, lds,
-                                                R_hi, R_lo, resid, n_iter, status, yvec);
+  k4_residual<T, CH><<<(unsigned)B, T, 0, st>>>(k, S, eps, Y, ldy, M, Mp, At, X, ldx, support, lds, R32,
+                                                (__nv_bfloat16*)Rb, R_hi, R_lo, resid, n_iter, status, yvec);
 }
 
 cudaError_t launch_residual(int32_t k, int32_t S, float eps, int64_t B, const float* Y, int64_t ldy,
                             int64_t M, int64_t Mp, const float* At, const float* X, int64_t ldx,
-                            const int32_t* support, int64_t lds, float* R_hi, float* R_lo,
+                            const int32_t* support, int64_t lds, float* R32, void* Rb, float* R_hi, float* R_lo,
                             float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const bool yvec = ((reinterpret_cast<uintptr_t>(Y) & 15) == 0) && (ldy % 4 == 0);
   const int64_t q4 = Mp / 4;
   if (q4 <= 32)
-    launch_k4<32, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<32, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else if (q4 <= 128)
-    launch_k4<128, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<128, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else if (q4 <= 256)
-    launch_k4<128, 2>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<128, 2>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else if (q4 <= 512)
-    launch_k4<128, 4>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<128, 4>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else if (q4 <= 1024)
-    launch_k4<128, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<128, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else if (q4 <= 2048)
-    launch_k4<256, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R_hi, R_lo, resid, n_iter, status, yvec, st);
+    launch_k4<256, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
   else
     return cudaErrorNotSupported;   // M > 8192
   return cudaGetLastError();

@@ -5,6 +5,9 @@
 // all stream-ordered on the caller's stream with no host synchronisation inside the loop
 // (SURVEY §3 "Ours", stack 2).  Finished signals keep their captured result and skip
 // K2-K4 (capture-and-continue).
+// Tensor-core modes: K1 is a screening GEMM (bf16 or 3xTF32 on tcgen05) whose epilogue keeps
+// top-4 candidates per 256-atom tile, and K2 re-evaluates every candidate inside the rigorous
+// screening window in exact FP32 (k_refine.cu).  SIMT mode: FP32 GEMM -> C -> argmax.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -27,14 +30,20 @@ struct ompHandle_st {
   int device = 0;
   int64_t M = 0, N = 0, Mp = 0, Np = 0;
   int mode = OMP_CORR_3XTF32;
-  // dictionary (owned): FP32 copy and TF32 planes of A^T (Np x Mp), 1/||a_n||, Gram (Np x Np)
+  float window = 0.f;      // screening window / ||r|| (tensor-core modes), DESIGN.md §5
+  // dictionary (owned): FP32 copy of A^T (Np x Mp), the screen's plane(s), 1/||a_n||, Gram
   float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *inv_norm = nullptr, *G = nullptr;
+  uint16_t* Ab = nullptr;  // bf16 plane
   int* dflags = nullptr;
   // batch workspace
   int64_t capB = 0;
   int32_t capS = 0;
-  float *R_hi = nullptr, *R_lo = nullptr, *C = nullptr, *P0 = nullptr, *F = nullptr, *U = nullptr;
+  float *R32 = nullptr, *R_hi = nullptr, *R_lo = nullptr, *C = nullptr, *F = nullptr, *U = nullptr;
+  uint16_t* Rb = nullptr;  // bf16 plane of the residuals
   int32_t* nstar = nullptr;
+  float* cstar = nullptr;
+  float2* part = nullptr;   // screening epilogue: (B) x (Np / 256) x TOPK candidates
+  int64_t capC = 0;         // rows of C (SIMT mode / ompCorrelate)
   int64_t ldf = 0, ldu = 0;
   int64_t lastB = 0;
   int32_t lastS = 0;
@@ -100,11 +109,30 @@ static cudaEvent_t take_event(ompHandle_t h) {
   return e;
 }
 
-// K1 dispatch: no silent fallback between modes
-static cudaError_t corr(ompHandle_t h, const Planes& R, float* C, int64_t ldc, cudaStream_t st) {
-  Planes At{h->At_hi, h->At_lo, h->Np, h->Mp};
-  if (h->mode == OMP_CORR_3XTF32) return launch_corr_tc(R, At, h->Mp, C, ldc, st);
-  return launch_corr_simt(R, At, h->Mp, C, ldc, st);
+static bool tc_mode(const ompHandle_t h) { return h->mode != OMP_CORR_FP32_SIMT; }
+static int tc_kind(const ompHandle_t h) { return h->mode == OMP_CORR_3XTF32 ? KIND_3XTF32 : KIND_BF16; }
+
+// operands of the mode's correlation kernel (no silent fallback between modes)
+static Operand atoms_operand(const ompHandle_t h) {
+  if (!tc_mode(h)) return Operand{{h->At, nullptr}, h->Np, h->Mp};
+  if (tc_kind(h) == KIND_BF16) return Operand{{h->Ab, nullptr}, h->Np, h->Mp};
+  return Operand{{h->At_hi, h->At_lo}, h->Np, h->Mp};
+}
+static Operand resid_operand(const ompHandle_t h, int64_t B) {
+  if (!tc_mode(h)) return Operand{{h->R32, nullptr}, B, h->Mp};
+  if (tc_kind(h) == KIND_BF16) return Operand{{h->Rb, nullptr}, B, h->Mp};
+  return Operand{{h->R_hi, h->R_lo}, B, h->Mp};
+}
+
+// rigorous screening bound c0 (|c~ - c| <= c0 ||a|| ||r||) + the FP32 re-evaluation bound,
+// doubled (both sides of the window) and padded by 25% for the FP32 norms
+static float screening_window(int mode, int64_t Kp) {
+  const double u23 = ldexp(1.0, -23);
+  double c0;
+  if (mode == OMP_CORR_3XTF32) c0 = ldexp(1.0, -20) + ldexp(1.0, -22) + 3.0 * (double)Kp * u23;
+  else c0 = ldexp(1.0, -8) + ldexp(1.0, -18) + (double)Kp * u23;   // bf16 operands
+  const double c_refine = ((double)Kp / 32.0 + 8.0) * u23;
+  return (float)(2.0 * (c0 + c_refine) * 1.25);
 }
 
 struct Launcher {
@@ -134,13 +162,17 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   const int64_t nB = B > h->capB ? B : h->capB;
   const int32_t nS = S > h->capS ? S : h->capS;
   const int64_t ldf = (int64_t)nS * (nS + 1) / 2;
-  bool ok = dalloc(h->R_hi, (size_t)nB * h->Mp) && dalloc(h->R_lo, (size_t)nB * h->Mp) &&
-            dalloc(h->C, (size_t)nB * h->Np) && dalloc(h->P0, (size_t)nB * h->Np) &&
-            dalloc(h->F, (size_t)nB * ldf) && dalloc(h->U, (size_t)nB * nS) &&
-            dalloc(h->nstar, (size_t)nB);
+  const bool tc = tc_mode(h), bf = tc && tc_kind(h) == KIND_BF16, x3 = tc && !bf;
+  bool ok = dalloc(h->R32, (size_t)nB * h->Mp) && dalloc(h->F, (size_t)nB * ldf) &&
+            dalloc(h->U, (size_t)nB * nS) && dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB);
+  if (ok && bf) ok = dalloc(h->Rb, (size_t)nB * h->Mp);
+  if (ok && x3) ok = dalloc(h->R_hi, (size_t)nB * h->Mp) && dalloc(h->R_lo, (size_t)nB * h->Mp);
+  if (ok && tc) ok = dalloc(h->part, (size_t)nB * (h->Np / N_TILE) * TOPK);
+  if (ok && !tc) ok = dalloc(h->C, (size_t)nB * h->Np);
+  h->capC = (ok && !tc) ? nB : 0;
   if (!ok) {
-    dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->P0); dfree(h->F); dfree(h->U);
-    dfree(h->nstar);
+    dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->F); dfree(h->U);
+    dfree(h->nstar); dfree(h->cstar); dfree(h->part); dfree(h->Rb);
     h->capB = 0;
     h->capS = 0;
     cudaGetLastError();
@@ -162,30 +194,45 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
   Launcher L{h, st};
   cudaError_t e;
   L.begin(0);
-  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, h->R_hi, h->R_lo, X, ldx, support, lds,
+  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, h->R32, h->Rb, h->R_hi, h->R_lo, X, ldx, support, lds,
                         resid, n_iter, status, st);
   L.end(0);
   if (e != cudaSuccess) return cuda_fail(h, e);
-  Planes R{h->R_hi, h->R_lo, B, h->Mp};
+  const Operand R = resid_operand(h, B), At = atoms_operand(h);
   for (int32_t k = 0; k < S; ++k) {
-    // a2: C = A^T R_k (k = 0: R_0 = Y, kept as P0 = A^T Y for the beta = a_{n*}^T y lookups)
-    float* Ck = (k == 0) ? h->P0 : h->C;
-    L.begin(1);
-    e = corr(h, R, Ck, h->Np, st);
-    L.end(1);
-    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
-    if (e != cudaSuccess) return cuda_fail(h, e);
-    L.begin(2);
-    e = launch_select(Ck, h->Np, B, h->N, h->inv_norm, status, h->nstar, st);
-    L.end(2);
-    if (e != cudaSuccess) return cuda_fail(h, e);
+    if (tc_mode(h)) {
+      // a2: tensor-core screen C~ = A^T R_k, epilogue -> top-4 candidates per 256-atom tile
+      L.begin(1);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->inv_norm, status, h->part, st);
+      L.end(1);
+      if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      // a3: exact FP32 argmax over the screening window
+      L.begin(2);
+      e = launch_refine(h->part, (int)(h->Np / N_TILE), B, h->N, h->Mp, h->R32, h->At, h->inv_norm, resid,
+                        h->window, status, h->nstar, h->cstar, st);
+      L.end(2);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    } else {
+      // a2: FP32 SIMT GEMM C = A^T R_k; a3: n* = argmax |c_n| / ||a_n||
+      L.begin(1);
+      e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, st);
+      L.end(1);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      L.begin(2);
+      e = launch_select(h->C, h->Np, B, h->N, h->inv_norm, status, h->nstar, h->cstar, st);
+      L.end(2);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    }
+    // a4: inverse-Cholesky factor append + coefficients
     L.begin(3);
-    e = launch_factor_append(k, B, h->nstar, h->G, h->Np, h->P0, h->Np, h->F, h->ldf, h->U, h->ldu,
-                             X, ldx, support, lds, status, st);
+    e = launch_factor_append(k, B, h->nstar, h->cstar, h->G, h->Np, h->F, h->ldf, h->U, h->ldu, X, ldx, support,
+                             lds, status, st);
     L.end(3);
     if (e != cudaSuccess) return cuda_fail(h, e);
+    // a5: residual, ||r||, eps mask, next operand planes
     L.begin(4);
-    e = launch_residual(k, S, eps, B, Y, ldy, h->M, h->Mp, h->At, X, ldx, support, lds, h->R_hi,
+    e = launch_residual(k, S, eps, B, Y, ldy, h->M, h->Mp, h->At, X, ldx, support, lds, h->R32, h->Rb, h->R_hi,
                         h->R_lo, resid, n_iter, status, st);
     L.end(4);
     if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
@@ -235,10 +282,10 @@ ompStatus_t ompDestroy(ompHandle_t h) {
   {
     DevGuard g(h->device);
     cudaDeviceSynchronize();
-    dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->inv_norm); dfree(h->G);
+    dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
-    dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->P0); dfree(h->F); dfree(h->U);
-    dfree(h->nstar);
+    dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
+    dfree(h->nstar); dfree(h->cstar); dfree(h->part);
     dfree(h->hY); dfree(h->hX); dfree(h->hres); dfree(h->hsup); dfree(h->hnit); dfree(h->hst);
     for (auto& r : h->prof_pending) {
       cudaEventDestroy(r.a);
@@ -255,7 +302,8 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   if (!out) return OMP_ERR_INVALID_ARG;
   *out = nullptr;
   if (!A || M < 1 || N < 1 || lda < M) return OMP_ERR_INVALID_ARG;
-  if (corr_mode != OMP_CORR_3XTF32 && corr_mode != OMP_CORR_FP32_SIMT) return OMP_ERR_INVALID_ARG;
+  if (corr_mode != OMP_CORR_BF16 && corr_mode != OMP_CORR_FP32_SIMT && corr_mode != OMP_CORR_3XTF32)
+    return OMP_ERR_INVALID_ARG;
   if (N > INT_MAX / 2) return OMP_ERR_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
@@ -272,10 +320,13 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   h->Mp = round_up(M, K_TILE);
   h->Np = round_up(N, N_TILE);
   h->mode = corr_mode;
+  h->window = screening_window(corr_mode, h->Mp);
   const size_t plane = (size_t)h->Np * h->Mp;
-  if (!(dalloc(h->At, plane) && dalloc(h->At_hi, plane) && dalloc(h->At_lo, plane) &&
-        dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
-        dalloc(h->dflags, 2))) {
+  bool ok = dalloc(h->At, plane) && dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
+            dalloc(h->dflags, 2);
+  if (ok && corr_mode == OMP_CORR_BF16) ok = dalloc(h->Ab, plane);
+  if (ok && corr_mode == OMP_CORR_3XTF32) ok = dalloc(h->At_hi, plane) && dalloc(h->At_lo, plane);
+  if (!ok) {
     ompDestroy(h);
     cudaGetLastError();
     return OMP_ERR_NOMEM;
@@ -283,7 +334,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   int init_flags[2] = {INT_MAX, INT_MAX};
   cudaError_t e = cudaMemcpyAsync(h->dflags, init_flags, sizeof(init_flags), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
-    e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->At_hi, h->At_lo, h->inv_norm,
+    e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->Ab, h->At_hi, h->At_lo, h->inv_norm,
                              h->dflags, h->dflags + 1, st);
   int flags[2] = {INT_MAX, INT_MAX};
   if (e == cudaSuccess) e = cudaMemcpyAsync(flags, h->dflags, sizeof(flags), cudaMemcpyDeviceToHost, st);
@@ -299,13 +350,13 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
     ompDestroy(h);
     return nonfinite ? OMP_ERR_NONFINITE : OMP_ERR_ZERO_COLUMN;
   }
-  // Gram matrix G = A^T A through the correlation kernel itself (R := A^T)
-  Planes R{h->At_hi, h->At_lo, h->Np, h->Mp};
-  e = corr(h, R, h->G, h->Np, st);
+  // Gram matrix G = A^T A in FP32 with round-to-nearest accumulation (the
+  // truncating tensor-core accumulator would bias ||a||^2 - ||z||^2)
+  const Operand A32{{h->At, nullptr}, h->Np, h->Mp};
+  e = launch_corr_simt(A32, A32, h->Mp, h->G, h->Np, h->Np, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
-    const bool unsup = e == cudaErrorNotSupported;
-    ompStatus_t s = unsup ? OMP_ERR_UNSUPPORTED : cuda_fail(nullptr, e);
+    ompStatus_t s = cuda_fail(nullptr, e);
     ompDestroy(h);
     return s;
   }
@@ -383,9 +434,18 @@ ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, 
   cudaStream_t st = (cudaStream_t)stream;
   ompStatus_t s = ensure_workspace(h, B, h->capS > 0 ? h->capS : 1);
   if (s != OMP_OK) return s;
-  cudaError_t e = launch_split_rows(R, B, ldr, h->M, h->Mp, h->R_hi, h->R_lo, st);
-  Planes P{h->R_hi, h->R_lo, B, h->Mp};
-  if (e == cudaSuccess) e = corr(h, P, h->C, h->Np, st);
+  if (B > h->capC) {
+    if (!dalloc(h->C, (size_t)B * h->Np)) {
+      h->capC = 0;
+      return OMP_ERR_NOMEM;
+    }
+    h->capC = B;
+  }
+  cudaError_t e = launch_make_planes(R, B, ldr, h->M, h->Mp, h->R32, h->Rb, h->R_hi, h->R_lo, st);
+  const Operand Rop = resid_operand(h, B), At = atoms_operand(h);
+  if (e == cudaSuccess)
+    e = tc_mode(h) ? launch_corr_tc(tc_kind(h), Rop, At, h->Mp, h->C, h->Np, h->Np, st)
+                   : launch_corr_simt(Rop, At, h->Mp, h->C, h->Np, h->Np, st);
   if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(C, ldc * sizeof(float), h->C, h->Np * sizeof(float), h->N * sizeof(float), B,
@@ -455,7 +515,7 @@ ompStatus_t omp_batch(const float* A, int64_t M, int64_t N, const float* Y, int6
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(nullptr, cudaGetLastError());
   ompHandle_t h = nullptr;
-  ompStatus_t s = ompCreate(&h, dev, A, M, N, M, OMP_CORR_3XTF32, stream);
+  ompStatus_t s = ompCreate(&h, dev, A, M, N, M, OMP_CORR_BF16, stream);
   if (s != OMP_OK) return s;
   s = ompBatch(h, Y, B, M, S, eps, X, S, support, S, resid, n_iter, status, stream);
   if (s == OMP_OK) {

@@ -18,7 +18,7 @@ from typing import Optional
 from . import _lib
 from ._lib import check
 
-MODES = {"3xtf32": _lib.OMP_CORR_3XTF32, "simt": _lib.OMP_CORR_FP32_SIMT}
+MODES = {"bf16": _lib.OMP_CORR_BF16, "simt": _lib.OMP_CORR_FP32_SIMT, "3xtf32": _lib.OMP_CORR_3XTF32}
 
 
 def _torch():
@@ -45,7 +45,7 @@ class OMPResult:
 class OMP:
     """A dictionary bound to one GPU (ompCreate): setup, Gram matrix and workspaces are cached."""
 
-    def __init__(self, A, mode: str = "3xtf32", stream=None):
+    def __init__(self, A, mode: str = "bf16", stream=None):
         torch = _torch()
         if not (isinstance(A, torch.Tensor) and A.is_cuda and A.dtype == torch.float32 and A.dim() == 2):
             raise TypeError("A must be a 2-D float32 CUDA tensor of shape (M, N)")
@@ -169,7 +169,7 @@ class OMP:
         return int(self.lib.ompGetLaunchCount(self.handle))
 
 
-def omp_batch(A, Y, S: int, eps: Optional[float] = None, mode: str = "3xtf32") -> OMPResult:
+def omp_batch(A, Y, S: int, eps: Optional[float] = None, mode: str = "bf16") -> OMPResult:
     """One-shot omp_batch(A, Y, S, eps) -> (X, support, resid_norm, n_iter, status)  (north star)."""
     with OMP(A, mode=mode) as h:
         return h.batch(Y, S, eps)

@@ -14,7 +14,7 @@ def eps32(eps):
     return None if eps is None else float(np.float32(eps))
 
 
-def run_gpu(A_np, Y_np, S, eps=None, mode="3xtf32", handle=None):
+def run_gpu(A_np, Y_np, S, eps=None, mode="bf16", handle=None):
     import torch
     from paper_2407_06434_b200 import OMP
     A = torch.from_numpy(A_np).cuda()

@@ -16,15 +16,29 @@ from oracle import DEGENERATE, EPS, MAXITER, NAN
 from synth import make_dictionary, make_problem, make_signals
 
 pytestmark = pytest.mark.gpu
-MODES = ["3xtf32", "simt"]
+MODES = ["bf16", "3xtf32", "simt"]
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
 
 
 # ------------------------------------------------------------------ correlation GEMM (K1)
+def screening_bound(mode, K):
+    """Rigorous |c~ - c| / (||a|| ||r||) of each correlation kernel: operand rounding
+    (bf16: 2 x 2^-9; 3xTF32: tf32-truncated lo terms + dropped lo*lo) plus at most one truncation
+    of the FP32 accumulator per product (K, or 3K for the three 3xTF32 products) times 2^-23."""
+    Kp = -(-K // 64) * 64
+    if mode == "bf16":
+        return 2.0 ** -8 + 2.0 ** -18 + Kp * 2.0 ** -23
+    if mode == "3xtf32":
+        return 2.0 ** -20 + 2.0 ** -22 + 3 * Kp * 2.0 ** -23
+    return 1e-6
+
+
 @pytest.mark.parametrize("mode", MODES)
-@pytest.mark.parametrize("shape", [(32, 64, 16), (256, 1024, 1000), (300, 700, 333), (1024, 4096, 520)])
+@pytest.mark.parametrize("shape", [(32, 64, 16), (256, 1024, 1000), (300, 700, 333), (1024, 4096, 520),
+                                   (2048, 8192, 1024)])
 def test_correlation_gemm_vs_fp64(mode, shape):
+    """K1 numerics: SIMT is FP32-accurate; the tensor-core screens stay inside their rigorous bound."""
     import torch
     from paper_2407_06434_b200 import OMP
     M, N, B = shape
@@ -37,13 +51,17 @@ def test_correlation_gemm_vs_fp64(mode, shape):
     ref = R.astype(np.float64) @ A.astype(np.float64)
     scale = np.linalg.norm(R, axis=1)[:, None] * np.linalg.norm(A, axis=0)[None, :]
     err = np.abs(C - ref) / scale
-    print(f"{mode} {shape}: max |C - C64| / (|r||a|) = {err.max():.3e}")
-    assert err.max() <= 1e-6
+    print(f"{mode} {shape}: max |C - C64| / (|r||a|) = {err.max():.3e}  bound {screening_bound(mode, M):.3e}")
+    if mode == "simt":
+        assert err.max() <= 1e-6
+    else:
+        # the bound is rigorous; with M >= 256 terms the rounding errors average well inside it
+        assert err.max() <= screening_bound(mode, M) * (0.5 if M >= 256 else 1.0)
     A64 = A.astype(np.float64)
     Gref = A64.T @ A64
     gs = np.linalg.norm(A, axis=0)
     gerr = np.abs(G - Gref) / (gs[:, None] * gs[None, :])
-    assert gerr.max() <= 1e-6
+    assert gerr.max() <= 1e-5   # G is FP32/round-to-nearest in every mode; diagonal = M same-sign terms
 
 
 # ------------------------------------------------------------------ worked examples (P5) on the GPU
@@ -97,7 +115,7 @@ def test_parity_c3_full_batch_sampled(mode):
 @pytest.mark.parametrize("B", [1, 10, 1000, 100000])
 def test_parity_c5_sweep_sampled(B):
     prob = make_problem("c5", B=B, device="cuda" if B > 1000 else None)
-    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "3xtf32")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
     rows = np.unique(np.linspace(0, B - 1, min(B, 48)).astype(int))
     assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), f"c5 B={B}")
 
@@ -105,7 +123,7 @@ def test_parity_c5_sweep_sampled(B):
 def test_parity_c4_full_batch_sampled():
     """BASELINE.json's largest config at its full size (B = 1e5), the bench's launch configuration."""
     prob = make_problem("c4", device="cuda")
-    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "3xtf32")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
     rows = [0, 1, 12499, 12500, 49999, 50000, 87499, 99999]
     assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), "c4")
     assert np.all(out["status"] == MAXITER) and np.all(out["n_iter"] == prob.S)
