@@ -135,9 +135,10 @@ ompStatus_t ompGetFactor(ompHandle_t handle, int64_t b0, int64_t count, float* F
                          void* stream);
 
 /* Profiling: when enabled, ompBatch brackets every kernel with CUDA events on `stream`;
- * ompProfileRead returns, per kernel slot (0 init, 1 correlation, 2 argmax, 3 factor
- * append, 4 residual), the summed milliseconds and the number of launches since the last
- * reset.  Reading synchronises the events.                                                */
+ * ompProfileRead returns, per kernel slot (0 init, 1 correlation, 2 standalone argmax [SIMT
+ * mode], 3 update = exact selection + factor append + residual, 4 reserved), the summed
+ * milliseconds and the number of launches since the last reset.  Reading synchronises the
+ * events.                                                                                  */
 #define OMP_NUM_KERNEL_SLOTS 5
 ompStatus_t ompProfileEnable(ompHandle_t handle, int enable);
 ompStatus_t ompProfileRead(ompHandle_t handle, double* ms, int64_t* launches, int reset);

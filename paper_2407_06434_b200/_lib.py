@@ -32,7 +32,7 @@ OMP_CORR_BF16 = 0
 OMP_CORR_FP32_SIMT = 1
 OMP_CORR_3XTF32 = 2
 OMP_NUM_KERNEL_SLOTS = 5
-KERNEL_SLOTS = ("init", "correlation", "select", "factor_append", "residual")
+KERNEL_SLOTS = ("init", "correlation", "select", "update", "reserved")
 
 # name -> (restype, argtypes); the list is also the ABI inventory tests check against the header
 SIGNATURES = {

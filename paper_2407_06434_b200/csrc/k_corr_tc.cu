@@ -191,6 +191,8 @@ struct EpiArgs {
   const float* inv_norm;    // MODE_TOPK
   float2* part;             // MODE_TOPK: rows x tiles_n x TOPK {value, index bits}
   const int32_t* status;    // MODE_TOPK: finished rows are skipped (may be null)
+  const float* resid;       // MODE_TOPK: ||r_b|| of the residual being screened
+  float window;             // MODE_TOPK: screening window / ||r||
 };
 
 struct Maps {
@@ -318,20 +320,12 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
       const int row = tm * BM * CG + (int)rank * BM + ew * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(a * BN);
       bool live = row < rows;
-      if constexpr (MODE == MODE_TOPK) {
-        if (live && ep.status) live = ep.status[row] == SIG_RUNNING;
-      }
-      float bv[TOPK];
-      int bi[TOPK];
-#pragma unroll
-      for (int j = 0; j < TOPK; ++j) { bv[j] = -1.f; bi[j] = -1; }
-      bool nan_seen = false;
+      if constexpr (MODE == MODE_STORE) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(taddr + (uint32_t)(c * 32), v);
-        const int64_t col0 = (int64_t)tn * BN + c * 32;
-        if constexpr (MODE == MODE_STORE) {
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + (uint32_t)(c * 32), v);
+          const int64_t col0 = (int64_t)tn * BN + c * 32;
           if (live) {
             float* dst = ep.C + (int64_t)row * ep.ldc + col0;
             if (col0 + 32 <= ep.ncols && (ep.ldc & 3) == 0) {
@@ -344,39 +338,65 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
                 if (col0 + q < ep.ncols) dst[q] = v[q];
             }
           }
-        } else {
-          if (live) {
-            const float4* w4 = reinterpret_cast<const float4*>(ep.inv_norm + col0);
+        }
+      } else {
+        // The refine kernel needs every atom within W = window ||r_b|| of the GLOBAL max; since the
+        // global max >= this tile's max, the entries within W of the tile max are a superset.
+        // Pass A: normalised chunk maxima (FMUL + FMNMX + FADD per value; the FADD sum is NaN iff
+        // some value is NaN, every term being >= 0).  Pass B: re-read only the chunks reaching
+        // tile_max - W and keep the top TOPK of those entries, in index order on ties.
+        float W = 0.f;
+        if (live && ep.status) live = ep.status[row] == SIG_RUNNING;
+        if (live) W = ep.window * ep.resid[row];
+        const float* wn = ep.inv_norm + (int64_t)tn * BN;
+        float cm[BN / 32];
+        float tmax = 0.f, csum = 0.f;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 w = __ldg(w4 + q);
-              const float wq[4] = {w.x, w.y, w.z, w.w};
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + (uint32_t)(c * 32), v);
+          float m = 0.f;
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float x = v[4 * q + e];
-                nan_seen |= isnan(x);
-                const float s = fabsf(x) * wq[e];
-                if (s > bv[TOPK - 1]) {        // insert, keeping equal values in index order
-                  float cv = s;
-                  int ci = (int)col0 + 4 * q + e;
+          for (int q = 0; q < 32; ++q) {
+            const float s = fabsf(v[q]) * __ldg(wn + c * 32 + q);
+            m = fmaxf(m, s);
+            csum += s;
+          }
+          cm[c] = m;
+          tmax = fmaxf(tmax, m);
+        }
+        const float thr = tmax - W;
+        float bv[TOPK];
+        int bi[TOPK];
 #pragma unroll
-                  for (int j = 0; j < TOPK; ++j) {
-                    if (cv > bv[j]) {
-                      const float tv = bv[j];
-                      const int ti = bi[j];
-                      bv[j] = cv; bi[j] = ci;
-                      cv = tv; ci = ti;
-                    }
+        for (int j = 0; j < TOPK; ++j) { bv[j] = -1.f; bi[j] = -1; }
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const bool need = live && cm[c] >= thr;
+          if (!__any_sync(0xffffffffu, need)) continue;       // warp-uniform: tcgen05.ld is .aligned
+          float v[32];
+          tmem_ld32(taddr + (uint32_t)(c * 32), v);
+          if (need) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              float cv = fabsf(v[q]) * __ldg(wn + c * 32 + q);
+              if (cv >= thr && cv > bv[TOPK - 1]) {
+                int ci = tn * BN + c * 32 + q;
+#pragma unroll
+                for (int j = 0; j < TOPK; ++j) {
+                  if (cv > bv[j]) {
+                    const float tv = bv[j];
+                    const int ti = bi[j];
+                    bv[j] = cv; bi[j] = ci;
+                    cv = tv; ci = ti;
                   }
                 }
               }
             }
           }
         }
-      }
-      if constexpr (MODE == MODE_TOPK) {
         if (live) {
-          if (nan_seen) bi[0] = SEL_NAN;
+          if (isnan(csum)) bi[0] = SEL_NAN;
           float4* dst = reinterpret_cast<float4*>(ep.part + ((int64_t)row * tiles_n + tn) * TOPK);
 #pragma unroll
           for (int j = 0; j < TOPK; j += 2)
@@ -500,13 +520,14 @@ static cudaError_t dispatch(int kind, const Operand& R, const Operand& At, int64
 
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, cudaStream_t st) {
-  tc::EpiArgs ep{C, ldc, ncols, nullptr, nullptr, nullptr};
+  tc::EpiArgs ep{C, ldc, ncols, nullptr, nullptr, nullptr, nullptr, 0.f};
   return tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
 }
 
 cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const float* inv_norm,
-                                const int32_t* status, float2* part, cudaStream_t st) {
-  tc::EpiArgs ep{nullptr, 0, At.rows, inv_norm, part, status};
+                                const int32_t* status, const float* resid, float window, float2* part,
+                                cudaStream_t st) {
+  tc::EpiArgs ep{nullptr, 0, At.rows, inv_norm, part, status, resid, window};
   return tc::dispatch<tc::MODE_TOPK>(kind, R, At, K, ep, st);
 }
 

@@ -1,17 +1,33 @@
-// K3: inverse-Cholesky factor append + coefficients, and
-// K4 (a5): residual gather r = y - A_S x, ||r||, eps mask, TF32 hi/lo planes of r.
+// The per-signal update of one OMP iteration, fused in one CTA per signal:
 //
-// K3 follows the paper's algorithm-v0 factor update:
-//   w = A_k^T a_{n*} = [A^T A]_{n*, S_k}    (Gram entries)
-//   z = F_k^T w,  gamma = 1/sqrt(||a_{n*}||^2 - ||z||^2)
-//   F_{k+1} = [[F_k, -gamma F_k z], [0, gamma]]                               (Eq. 8)
-//   u = F^T A^T y grows by u_new = f^T A_{k+1}^T y = gamma a_{n*}^T r_k = gamma c*
-//     (the new basis vector q = A_{k+1} f is orthogonal to span A_k, so q^T y = q^T r_k; pin P9)
-//   x = F_{k+1} u  (matrix-vector products only, Eq. 11)
-// F is upper triangular and packed by columns (column j = F[0..j, j] at offset j(j+1)/2),
-// the paper's packed representation applied to the factor, so the
-// leading block is a contiguous prefix and appending a column is a contiguous write.
-// Every live signal is at the same k (= iteration), so k is a kernel argument.
+//  a3  (REFINE = true, tensor-core modes) exact selection after the screen:
+//        n*_b = lowest n maximising |<r_b, a_n>| / ||a_n||
+//      The screen (k_corr_tc.cu) bounds |c~_n - c_n| <= c0 ||a_n|| ||r_b||, i.e. c0 ||r_b|| in
+//      normalised units for every n, so the exact argmax lies in
+//        { n : v~_n >= max v~ - window ||r_b|| },  window = 2 (c0 + c0')   (c0' bounds this FP32 dot).
+//      The screen kept, per 256-atom tile, the top-4 entries within the window of the tile max; a
+//      tile whose 4th kept entry is still inside the global window is re-evaluated in full, an
+//      overfull candidate list falls back to all N atoms.  Every candidate is re-evaluated as an
+//      FP32 dot of the fp32 residual and the fp32 atom in a fixed order.  (REFINE = false: n*, c*
+//      come from the standalone argmax over a materialised FP32 C, k_select.cu.)
+//
+//  a4  inverse-Cholesky factor append, the paper's algorithm-v0 update:
+//        w = A_k^T a_{n*} = [A^T A]_{n*, S_k}
+//        z = F_k^T w,  gamma = 1/sqrt(||a_{n*}||^2 - ||z||^2)
+//        F_{k+1} = [[F_k, -gamma F_k z], [0, gamma]]                               (Eq. 8)
+//        u = F^T A^T y grows by u_new = gamma <r_k, a_{n*}> = gamma c*  (q = A_{k+1} f is orthogonal
+//            to span A_k, so q^T y = q^T r_k; pin P9)
+//        x = F_{k+1} u   (matrix-vector products only, Eq. 11)
+//      F is upper triangular, packed by columns (column j = F[0..j, j] at offset j(j+1)/2), the
+//      paper's packed representation: the leading block is a contiguous prefix,
+//      staged into shared memory by one cp.async.bulk at kernel start, so F leaves HBM once per
+//      iteration and both passes over it run from shared memory.
+//
+//  a5  residual r_b = y_b - sum_{j<=k} x_j a_{s_j} from gathered atom rows of A^T,
+//      ||r_b||, the eps test, and the operand planes of the next screen.
+//
+// Every live signal is at the same k (= iteration), so k is a kernel argument.  Finished signals
+// return at once (capture-and-continue).
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -19,10 +35,63 @@
 
 namespace ompb {
 
+constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N atoms)
+
+struct UpdateArgs {
+  int32_t k, S;
+  float eps;
+  int64_t N, M, Mp;
+  // selection inputs
+  const float2* part;   // screen partials (REFINE)
+  int tiles_n;
+  float window;
+  const int32_t* nstar; // preselected (SIMT mode)
+  const float* cstar;
+  // dictionary
+  const float* At;      // fp32 atom rows (Np x Mp)
+  const float* inv_norm;
+  const float* G;       // Gram matrix, row stride ldg
+  int64_t ldg;
+  // per-signal state
+  const float* Y;
+  int64_t ldy;
+  float* F;
+  int64_t ldf;
+  float* U;
+  int64_t ldu;
+  float* X;
+  int64_t ldx;
+  int32_t* support;
+  int64_t lds;
+  float* R32;
+  __nv_bfloat16* Rb;
+  float* Rhi;
+  float* Rlo;
+  float* resid;
+  int32_t* n_iter;
+  int32_t* status;
+  int f_stage;          // 1: stage F_k in shared memory (else read F from global)
+  int region_floats;    // floats of the aliased residual-row / F region
+};
+
+struct Cand {
+  float w;
+  int n;
+  float c;
+};
+
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {   // is a better than b
+  return a.w > b.w || (a.w == b.w && a.n < b.n);
+}
+
 __device__ __forceinline__ float tf32_rna_u(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 template <int T>
@@ -38,36 +107,186 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return r;
 }
 
-template <int T>
-__global__ void __launch_bounds__(T) k3_factor_append(
-    int32_t k, const int32_t* __restrict__ nstar, const float* __restrict__ cstar, const float* __restrict__ G,
-    int64_t ldg, float* __restrict__ F, int64_t ldf,
-    float* __restrict__ U, int64_t ldu, float* __restrict__ X, int64_t ldx,
-    int32_t* __restrict__ support, int64_t lds, int32_t* __restrict__ status) {
+// lanes of one warp: c = sum_m r[m] a_n[m] in a fixed order (lane-strided float4, xor tree)
+__device__ __forceinline__ float warp_dot(const float4* __restrict__ r4, const float4* __restrict__ a4, int q4,
+                                          int lane) {
+  float acc = 0.f;
+  for (int q = lane; q < q4; q += 32) {
+    const float4 a = __ldg(a4 + q);
+    const float4 r = r4[q];
+    acc = fmaf(r.x, a.x, acc);
+    acc = fmaf(r.y, a.y, acc);
+    acc = fmaf(r.z, a.z, acc);
+    acc = fmaf(r.w, a.w, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+template <bool REFINE, int T, int CH>
+__global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   const int64_t b = blockIdx.x;
-  if (status[b] != SIG_RUNNING) return;
-  const int n = nstar[b];
-  if (n < 0) {   // exhausted residual or non-finite correlations (K2)
-    if (threadIdx.x == 0) status[b] = (n == SEL_NAN) ? OMP_SIG_NAN : OMP_SIG_DEGENERATE;
+  if (a.status[b] != SIG_RUNNING) return;
+  const int k = a.k;
+  const int q4 = (int)(a.Mp >> 2);
+  const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
+  // dynamic shared memory (sizes in launch_update):
+  //   [region X: the fp32 residual row (refine) then the packed F_k prefix (append), aliased]
+  //   [w, z, u, xs: Sp floats each] [ss: Sp ints] [cand: RF_CAP ints (refine)]
+  extern __shared__ __align__(16) uint8_t dsm[];
+  float4* rsm = reinterpret_cast<float4*>(dsm);
+  float* Fs = reinterpret_cast<float*>(dsm);
+  float* w = reinterpret_cast<float*>(dsm + (size_t)a.region_floats * 4);
+  float* z = w + Sp;
+  float* u = z + Sp;
+  float* xs = u + Sp;
+  int* ss = reinterpret_cast<int*>(xs + Sp);
+  int* cand = ss + Sp;
+  __shared__ float red[T / 32];
+  __shared__ Cand red_c[T / 32];
+  __shared__ int ncand;
+  __shared__ int sel_n;
+  __shared__ float sel_c;
+  __shared__ __align__(8) uint64_t fbar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* Fg = a.F + b * a.ldf;
+  const uint32_t fbytes = (uint32_t)((((int64_t)k * (k + 1) / 2) + 3) / 4 * 16);
+  const bool staged = a.f_stage && fbytes > 0;
+  bool issued = false;
+  if (tid == 0) {
+    ncand = 0;
+    if (staged) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&fbar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+
+  // ---- a3: selection ------------------------------------------------------------------------------
+  if constexpr (REFINE) {
+    const float rn = a.resid[b];
+    const float2* P = a.part + b * (int64_t)a.tiles_n * TOPK;
+    const int E = a.tiles_n * TOPK;
+    float vmax = -1.f;
+    bool nan_seen = false;
+    for (int e = tid; e < E; e += T) {
+      const float2 p = P[e];
+      nan_seen |= (__float_as_int(p.y) == SEL_NAN) | isnan(p.x);
+      vmax = fmaxf(vmax, p.x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if (lane == 0) red[warp] = vmax;
+    const int any_nan = __syncthreads_or(nan_seen || !isfinite(rn));
+    if (any_nan) {
+      if (tid == 0) a.status[b] = OMP_SIG_NAN;
+      return;
+    }
+    if (rn == 0.f) {                                   // r = 0 exactly: every correlation is 0
+      if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
+      return;
+    }
+    vmax = red[0];
+#pragma unroll
+    for (int i = 1; i < T / 32; ++i) vmax = fmaxf(vmax, red[i]);
+    const float thr = vmax - a.window * rn;
+    bool full = false;
+    for (int t = tid; t < a.tiles_n; t += T) {
+      if (P[t * TOPK + TOPK - 1].x >= thr) {            // tile may hold more candidates: all of it
+        const int n0 = t * N_TILE;
+        const int cnt = (int)min((int64_t)N_TILE, a.N - n0);
+        if (cnt > 0) {
+          const int at = atomicAdd(&ncand, cnt);
+          if (at + cnt > RF_CAP) full = true;
+          else
+            for (int i = 0; i < cnt; ++i) cand[at + i] = n0 + i;
+        }
+      } else {
+        for (int j = 0; j < TOPK; ++j) {
+          const float2 p = P[t * TOPK + j];
+          const int n = __float_as_int(p.y);
+          if (p.x >= thr && n >= 0 && n < a.N) {
+            const int at = atomicAdd(&ncand, 1);
+            if (at >= RF_CAP) full = true;
+            else cand[at] = n;
+          }
+        }
+      }
+    }
+    const float4* r4g = reinterpret_cast<const float4*>(a.R32 + b * a.Mp);
+    for (int q = tid; q < q4; q += T) rsm[q] = r4g[q];
+    full = __syncthreads_or(full);
+    Cand best{-1.f, 0x7fffffff, 0.f};
+    const int count = full ? (int)a.N : min(ncand, RF_CAP);
+    for (int j = warp; j < count; j += T / 32) {
+      const int n = full ? j : cand[j];
+      const float c = warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane);
+      const Cand cd{fabsf(c) * a.inv_norm[n], n, c};
+      if (cand_better(cd, best)) best = cd;
+    }
+    if (lane == 0) red_c[warp] = best;
+    __syncthreads();                                    // residual row no longer needed past here
+    if (tid == 0) {
+      Cand r = red_c[0];
+#pragma unroll
+      for (int i = 1; i < T / 32; ++i)
+        if (cand_better(red_c[i], r)) r = red_c[i];
+      const bool ok = r.w > 0.f && r.n < a.N;
+      sel_n = ok ? r.n : SEL_DEGENERATE;
+      sel_c = ok ? r.c : 0.f;
+    }
+  } else {
+    if (tid == 0) {
+      sel_n = a.nstar[b];
+      sel_c = a.cstar[b];
+    }
+  }
+  // stage F_k (the contiguous packed prefix) over the freed residual-row region, asynchronously;
+  // it lands while the support, the Gram entries and u are gathered below
+  if (tid == 0 && staged && sel_n >= 0) {
+    // order the generic-proxy reads of the residual row before the async-proxy overwrite
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&fbar)), "r"(fbytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(Fs)), "l"(Fg), "r"(fbytes), "r"(smem_addr(&fbar))
+                 : "memory");
+  }
+  __syncthreads();
+  const int n = sel_n;
+  const float cst = sel_c;
+  if (n < 0) {
+    if (tid == 0) a.status[b] = (n == SEL_NAN) ? OMP_SIG_NAN : OMP_SIG_DEGENERATE;
     return;
   }
-  __shared__ float w[MAX_S], z[MAX_S], u[MAX_S];
-  __shared__ float red[T / 32];
-  const float* grow = G + (int64_t)n * ldg;
+  issued = staged;
+  auto wait_f = [&]() {
+    if (!issued) return;
+    uint32_t ok = 0;
+    do {
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                   "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_addr(&fbar)) : "memory");
+    } while (!ok);
+  };
+
+  // ---- a4: factor append --------------------------------------------------------------------------
+  const float* grow = a.G + (int64_t)n * a.ldg;
   bool dup = false;
-  for (int j = threadIdx.x; j < k; j += T) {
-    const int s = support[b * lds + j];
+  for (int j = tid; j < k; j += T) {
+    const int s = a.support[b * a.lds + j];
+    ss[j] = s;
     dup |= (s == n);
     w[j] = grow[s];                     // [A^T A]_{n*, s_j}
-    u[j] = U[b * ldu + j];
+    u[j] = a.U[b * a.ldu + j];
   }
-  if (__syncthreads_or(dup)) {          // re-selection (reading R6)
-    if (threadIdx.x == 0) status[b] = OMP_SIG_DEGENERATE;
+  if (__syncthreads_or(dup)) {          // re-selection (reading R6); let the F copy land first
+    wait_f();
+    if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
     return;
   }
-  float* Fb = F + b * ldf;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // z_j = F[:, j] . w  (column dot, one warp per column, coalesced)
+  wait_f();
+  const float* Fb = staged ? Fs : Fg;
+  // z_j = F[:, j] . w  (column dot, one warp per column)
   for (int j = warp; j < k; j += T / 32) {
     const float* col = Fb + (int64_t)j * (j + 1) / 2;
     float acc = 0.f;
@@ -78,165 +297,174 @@ __global__ void __launch_bounds__(T) k3_factor_append(
   }
   __syncthreads();
   float zz = 0.f;
-  for (int j = threadIdx.x; j < k; j += T) zz = fmaf(z[j], z[j], zz);
+  for (int j = tid; j < k; j += T) zz = fmaf(z[j], z[j], zz);
   zz = block_sum<T>(zz, red);
   const float d = grow[n];              // ||a_{n*}||^2
   const float delta = d - zz;
   if (!(delta > TAU_F * d)) {           // rank deficiency (reading R6); also catches NaN
-    if (threadIdx.x == 0) status[b] = OMP_SIG_DEGENERATE;
+    if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
     return;
   }
   const float gamma = 1.0f / sqrtf(delta);
-  const float unew = gamma * cstar[b];  // gamma <r_k, a_{n*}>
-  // v = F_k z and t = F_k u in one pass over F (thread per row, coalesced per column)
-  float* newcol = Fb + (int64_t)k * (k + 1) / 2;
-  for (int i = threadIdx.x; i < k; i += T) {
+  const float unew = gamma * cst;       // gamma <r_k, a_{n*}>
+  // v = F_k z and t = F_k u in one pass over F (thread per row; lanes of a warp share column j)
+  float* newcol = a.F + b * a.ldf + (int64_t)k * (k + 1) / 2;
+  for (int i = tid; i < k; i += T) {
     float v = 0.f, t = 0.f;
-    // lanes of a warp walk the same column j together (i & ~31 = warp's first row)
     for (int j = i & ~31; j < k; ++j) {
       const float f = (j >= i) ? Fb[(int64_t)j * (j + 1) / 2 + i] : 0.f;
       v = fmaf(f, z[j], v);
       t = fmaf(f, u[j], t);
     }
     newcol[i] = -gamma * v;                       // -gamma F_k z
-    X[b * ldx + i] = fmaf(-gamma * v, unew, t);   // x_i = (F_k u)_i + f_i u_new
+    const float xi = fmaf(-gamma * v, unew, t);   // x_i = (F_k u)_i + f_i u_new
+    a.X[b * a.ldx + i] = xi;
+    xs[i] = xi;
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     newcol[k] = gamma;
-    X[b * ldx + k] = gamma * unew;
-    U[b * ldu + k] = unew;
-    support[b * lds + k] = n;
-  }
-}
-
-cudaError_t launch_factor_append(int32_t k, int64_t B, const int32_t* nstar, const float* cstar, const float* G,
-                                 int64_t ldg, float* F, int64_t ldf, float* u, int64_t ldu, float* X, int64_t ldx,
-                                 int32_t* support, int64_t lds, int32_t* status, cudaStream_t st) {
-  if (B == 0) return cudaSuccess;
-  k3_factor_append<128><<<(unsigned)B, 128, 0, st>>>(k, nstar, cstar, G, ldg, F, ldf, u, ldu, X, ldx, support, lds,
-                                                     status);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------------------
-// K4: r_b = y_b - sum_{j<=k} x_j a_{s_j}, gathered atom rows of A^T.
-// Thread t owns CH float4 chunks of r (m = 4(t + c T)); atoms are streamed in the outer
-// loop so the CH loads of one atom row are independent (memory-level parallelism).
-// ---------------------------------------------------------------------------------------
-template <int T, int CH>
-__global__ void __launch_bounds__(T) k4_residual(
-    int32_t k, int32_t S, float eps, const float* __restrict__ Y, int64_t ldy, int64_t M, int64_t Mp,
-    const float* __restrict__ At, const float* __restrict__ X, int64_t ldx,
-    const int32_t* __restrict__ support, int64_t lds, float* __restrict__ R32, __nv_bfloat16* __restrict__ Rb,
-    float* __restrict__ R_hi, float* __restrict__ R_lo, float* __restrict__ resid, int32_t* __restrict__ n_iter,
-    int32_t* __restrict__ status, bool yvec) {
-  const int64_t b = blockIdx.x;
-  if (status[b] != SIG_RUNNING) return;
-  __shared__ float xs[MAX_S];
-  __shared__ int ss[MAX_S];
-  __shared__ float red[T / 32];
-  const int kk = k + 1;
-  for (int j = threadIdx.x; j < kk; j += T) {
-    xs[j] = X[b * ldx + j];
-    ss[j] = support[b * lds + j];
+    const float xk = gamma * unew;
+    a.X[b * a.ldx + k] = xk;
+    xs[k] = xk;
+    ss[k] = n;
+    a.U[b * a.ldu + k] = unew;
+    a.support[b * a.lds + k] = n;
   }
   __syncthreads();
-  const int64_t q4 = Mp >> 2;   // float4 chunks per row
+
+  // ---- a5: residual r = y - A_S x, ||r||, eps test, next screening operand ------------------------
+  // The gather is L2-bandwidth bound: every thread keeps 4 atoms x CH float4 loads in flight.
+  const int kk = k + 1;
   float4 acc[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* A4 = reinterpret_cast<const float4*>(At);
-#pragma unroll 2
-  for (int j = 0; j < kk; ++j) {
+  const float4* A4 = reinterpret_cast<const float4*>(a.At);
+  int j = 0;
+  for (; j + 4 <= kk; j += 4) {
+    float4 av[4][CH];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float4* row = A4 + (int64_t)ss[j + t] * q4;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int q = tid + c * T;
+        av[t][c] = q < q4 ? __ldg(row + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float xj = xs[j + t];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        acc[c].x = fmaf(xj, av[t][c].x, acc[c].x);
+        acc[c].y = fmaf(xj, av[t][c].y, acc[c].y);
+        acc[c].z = fmaf(xj, av[t][c].z, acc[c].z);
+        acc[c].w = fmaf(xj, av[t][c].w, acc[c].w);
+      }
+    }
+  }
+  for (; j < kk; ++j) {
     const float xj = xs[j];
     const float4* row = A4 + (int64_t)ss[j] * q4;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const int64_t q = threadIdx.x + (int64_t)c * T;
+      const int q = tid + c * T;
       if (q < q4) {
-        const float4 a = __ldg(row + q);
-        acc[c].x = fmaf(xj, a.x, acc[c].x);
-        acc[c].y = fmaf(xj, a.y, acc[c].y);
-        acc[c].z = fmaf(xj, a.z, acc[c].z);
-        acc[c].w = fmaf(xj, a.w, acc[c].w);
+        const float4 av = __ldg(row + q);
+        acc[c].x = fmaf(xj, av.x, acc[c].x);
+        acc[c].y = fmaf(xj, av.y, acc[c].y);
+        acc[c].z = fmaf(xj, av.z, acc[c].z);
+        acc[c].w = fmaf(xj, av.w, acc[c].w);
       }
     }
   }
-  const float* y = Y + b * ldy;
+  const float* y = a.Y + b * a.ldy;
+  const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
   float part = 0.f;
-  float4* R4 = reinterpret_cast<float4*>(R32 + b * Mp);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    const int64_t q = threadIdx.x + (int64_t)c * T;
+    const int q = tid + c * T;
     if (q < q4) {
-      const int64_t m = q << 2;
+      const int64_t m = (int64_t)q << 2;
       float4 yv;
-      if (yvec && m + 3 < M) {
+      if (yvec && m + 3 < a.M) {
         yv = __ldcs(reinterpret_cast<const float4*>(y + m));
       } else {
-        yv.x = m < M ? y[m] : 0.f;
-        yv.y = m + 1 < M ? y[m + 1] : 0.f;
-        yv.z = m + 2 < M ? y[m + 2] : 0.f;
-        yv.w = m + 3 < M ? y[m + 3] : 0.f;
+        yv.x = m < a.M ? y[m] : 0.f;
+        yv.y = m + 1 < a.M ? y[m + 1] : 0.f;
+        yv.z = m + 2 < a.M ? y[m + 2] : 0.f;
+        yv.w = m + 3 < a.M ? y[m + 3] : 0.f;
       }
-      float4 r = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
+      const float4 r = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
       part = fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, fmaf(r.w, r.w, part))));
-      R4[q] = r;
-      if (Rb) {
+      if (a.R32) reinterpret_cast<float4*>(a.R32 + b * a.Mp)[q] = r;
+      if (a.Rb) {
         __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&p0);
         pk.y = *reinterpret_cast<uint32_t*>(&p1);
-        reinterpret_cast<uint2*>(Rb + b * Mp)[q] = pk;
+        reinterpret_cast<uint2*>(a.Rb + b * a.Mp)[q] = pk;
       }
-      if (R_hi) {
+      if (a.Rhi) {
         const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
-        reinterpret_cast<float4*>(R_hi + b * Mp)[q] = h;
-        reinterpret_cast<float4*>(R_lo + b * Mp)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
+        reinterpret_cast<float4*>(a.Rhi + b * a.Mp)[q] = h;
+        reinterpret_cast<float4*>(a.Rlo + b * a.Mp)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
       }
     }
   }
   const float rr = block_sum<T>(part, red);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const float rn = sqrtf(rr);
-    resid[b] = rn;
-    n_iter[b] = kk;
-    if (eps >= 0.f && rn <= eps) status[b] = OMP_SIG_EPS;
-    else if (kk == S) status[b] = OMP_SIG_MAXITER;
+    a.resid[b] = rn;
+    a.n_iter[b] = kk;
+    if (a.eps >= 0.f && rn <= a.eps) a.status[b] = OMP_SIG_EPS;
+    else if (kk == a.S) a.status[b] = OMP_SIG_MAXITER;
   }
 }
 
-template <int T, int CH>
-static void launch_k4(int32_t k, int32_t S, float eps, int64_t B, const float* Y, int64_t ldy, int64_t M,
-                      int64_t Mp, const float* At, const float* X, int64_t ldx, const int32_t* support,
-                      int64_t lds, float* R32, void* Rb, float* R_hi, float* R_lo, float* resid, int32_t* n_iter,
-                      int32_t* status, bool yvec, cudaStream_t st) {
-  k4_residual<T, CH><<<(unsigned)B, T, 0, st>>>(k, S, eps, Y, ldy, M, Mp, At, X, ldx, support, lds, R32,
-                                                (__nv_bfloat16*)Rb, R_hi, R_lo, resid, n_iter, status, yvec);
+template <bool REFINE, int T, int CH>
+static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, cudaStream_t st) {
+  auto kern = k_update<REFINE, T, CH>;
+  // static (~12 KB) + dynamic shared memory may exceed the 48 KB default: opt in once per variant
+  static bool opted = false;
+  if (!opted) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return e;
+    opted = true;
+  }
+  kern<<<(unsigned)B, T, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_residual(int32_t k, int32_t S, float eps, int64_t B, const float* Y, int64_t ldy,
-                            int64_t M, int64_t Mp, const float* At, const float* X, int64_t ldx,
-                            const int32_t* support, int64_t lds, float* R32, void* Rb, float* R_hi, float* R_lo,
-                            float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
-  if (B == 0) return cudaSuccess;
-  const bool yvec = ((reinterpret_cast<uintptr_t>(Y) & 15) == 0) && (ldy % 4 == 0);
-  const int64_t q4 = Mp / 4;
-  if (q4 <= 32)
-    launch_k4<32, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else if (q4 <= 128)
-    launch_k4<128, 1>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else if (q4 <= 256)
-    launch_k4<128, 2>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else if (q4 <= 512)
-    launch_k4<128, 4>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else if (q4 <= 1024)
-    launch_k4<128, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else if (q4 <= 2048)
-    launch_k4<256, 8>(k, S, eps, B, Y, ldy, M, Mp, At, X, ldx, support, lds, R32, Rb, R_hi, R_lo, resid, n_iter, status, yvec, st);
-  else
-    return cudaErrorNotSupported;   // M > 8192
-  return cudaGetLastError();
+template <bool REFINE>
+static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, cudaStream_t st) {
+  const int64_t q4 = a.Mp / 4;
+  if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, st);
+  if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, st);
+  if (q4 <= 512) return launch_t<REFINE, 128, 4>(a, B, smem, st);
+  if (q4 <= 1024) return launch_t<REFINE, 256, 4>(a, B, smem, st);
+  if (q4 <= 2048) return launch_t<REFINE, 256, 8>(a, B, smem, st);
+  return cudaErrorNotSupported;   // M > 8192
+}
+
+cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
+  if (L.B == 0) return cudaSuccess;
+  UpdateArgs a;
+  a.k = L.k; a.S = L.S; a.eps = L.eps; a.N = L.N; a.M = L.M; a.Mp = L.Mp;
+  a.part = L.part; a.tiles_n = L.tiles_n; a.window = L.window; a.nstar = L.nstar; a.cstar = L.cstar;
+  a.At = L.At; a.inv_norm = L.inv_norm; a.G = L.G; a.ldg = L.ldg;
+  a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
+  a.support = L.support; a.lds = L.lds; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb; a.Rhi = L.Rhi;
+  a.Rlo = L.Rlo; a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status;
+  // one region holds the residual row (refine) and then F_k (append); F is staged when it fits
+  const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) / 4 * 4;
+  const bool refine = L.part != nullptr;
+  const int64_t rowf = refine ? L.Mp : 0;
+  a.f_stage = (fk * 4 <= (int64_t)64 * 1024 && L.ldf % 4 == 0) ? 1 : 0;
+  a.region_floats = (int)((a.f_stage && fk > rowf) ? fk : rowf);
+  const int64_t Sp = (L.k + 4) & ~3;
+  const size_t smem = (size_t)a.region_floats * 4 + (size_t)Sp * 5 * 4 + (refine ? RF_CAP * 4 : 0);
+  return refine ? launch_r<true>(a, L.B, smem, st) : launch_r<false>(a, L.B, smem, st);
 }
 
 }  // namespace ompb

@@ -161,7 +161,7 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   if (B <= h->capB && S <= h->capS) return OMP_OK;
   const int64_t nB = B > h->capB ? B : h->capB;
   const int32_t nS = S > h->capS ? S : h->capS;
-  const int64_t ldf = (int64_t)nS * (nS + 1) / 2;
+  const int64_t ldf = round_up((int64_t)nS * (nS + 1) / 2, 4);   // 16-byte aligned rows for the bulk copy
   const bool tc = tc_mode(h), bf = tc && tc_kind(h) == KIND_BF16, x3 = tc && !bf;
   bool ok = dalloc(h->R32, (size_t)nB * h->Mp) && dalloc(h->F, (size_t)nB * ldf) &&
             dalloc(h->U, (size_t)nB * nS) && dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB);
@@ -201,20 +201,15 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
   const Operand R = resid_operand(h, B), At = atoms_operand(h);
   for (int32_t k = 0; k < S; ++k) {
     if (tc_mode(h)) {
-      // a2: tensor-core screen C~ = A^T R_k, epilogue -> top-4 candidates per 256-atom tile
+      // a2: tensor-core screen C~ = A^T R_k; the epilogue keeps per 256-atom tile the top-4 entries
+      // within the screening window of the tile maximum
       L.begin(1);
-      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->inv_norm, status, h->part, st);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->inv_norm, status, resid, h->window, h->part, st);
       L.end(1);
       if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
       if (e != cudaSuccess) return cuda_fail(h, e);
-      // a3: exact FP32 argmax over the screening window
-      L.begin(2);
-      e = launch_refine(h->part, (int)(h->Np / N_TILE), B, h->N, h->Mp, h->R32, h->At, h->inv_norm, resid,
-                        h->window, status, h->nstar, h->cstar, st);
-      L.end(2);
-      if (e != cudaSuccess) return cuda_fail(h, e);
     } else {
-      // a2: FP32 SIMT GEMM C = A^T R_k; a3: n* = argmax |c_n| / ||a_n||
+      // a2: FP32 SIMT GEMM C = A^T R_k; a3: n* = argmax |c_n| / ||a_n|| over the materialised C
       L.begin(1);
       e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, st);
       L.end(1);
@@ -224,17 +219,22 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
       L.end(2);
       if (e != cudaSuccess) return cuda_fail(h, e);
     }
-    // a4: inverse-Cholesky factor append + coefficients
+    // a3 (tensor-core modes: exact re-evaluation of the screen's candidates) + a4 factor append +
+    // a5 residual / eps mask / next operand planes, one CTA per live signal
+    UpdateLaunch U;
+    U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
+    U.part = tc_mode(h) ? h->part : nullptr;
+    U.tiles_n = (int)(h->Np / N_TILE);
+    U.window = h->window;
+    U.nstar = h->nstar; U.cstar = h->cstar;
+    U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
+    U.Y = Y; U.ldy = ldy; U.F = h->F; U.ldf = h->ldf; U.U = h->U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
+    U.support = support; U.lds = lds;
+    U.R32 = h->R32; U.Rb = h->Rb; U.Rhi = h->R_hi; U.Rlo = h->R_lo;
+    U.resid = resid; U.n_iter = n_iter; U.status = status;
     L.begin(3);
-    e = launch_factor_append(k, B, h->nstar, h->cstar, h->G, h->Np, h->F, h->ldf, h->U, h->ldu, X, ldx, support,
-                             lds, status, st);
+    e = launch_update(U, st);
     L.end(3);
-    if (e != cudaSuccess) return cuda_fail(h, e);
-    // a5: residual, ||r||, eps mask, next operand planes
-    L.begin(4);
-    e = launch_residual(k, S, eps, B, Y, ldy, h->M, h->Mp, h->At, X, ldx, support, lds, h->R32, h->Rb, h->R_hi,
-                        h->R_lo, resid, n_iter, status, st);
-    L.end(4);
     if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
     if (e != cudaSuccess) return cuda_fail(h, e);
   }

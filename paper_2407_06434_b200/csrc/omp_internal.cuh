@@ -44,19 +44,16 @@ cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, flo
 // tcgen05 screening GEMM, C~ stored (diagnostics / numerics tests)
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, cudaStream_t st);
-// tcgen05 screening GEMM, epilogue -> top-TOPK (|c~| / ||a||, n) per (row, 256-atom tile)
+// tcgen05 screening GEMM, epilogue -> per (row, 256-atom tile) the top-TOPK (|c~| / ||a||, n) among
+// the entries within window * resid[row] of the tile's maximum
 cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const float* inv_norm,
-                                const int32_t* status, float2* part, cudaStream_t st);
+                                const int32_t* status, const float* resid, float window, float2* part,
+                                cudaStream_t st);
 
 // ---- K2 ----
 // a3 over a materialised FP32 C: n*_b = lowest n maximising |C[b,n]| * inv_norm[n]; c* = C[b, n*]
 cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, const float* inv_norm,
                           const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st);
-// a3 after the screen: exact FP32 re-evaluation of every candidate within `window` * ||r_b||
-cudaError_t launch_refine(const float2* part, int tiles_n, int64_t B, int64_t N, int64_t Mp,
-                          const float* R32, const float* At, const float* inv_norm, const float* resid,
-                          float window, const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st);
-
 // ---- setup / init ----
 // K0: atoms -> FP32 copy At (Np x Mp), optional bf16 plane / tf32 hi-lo planes, 1/||a_n||
 cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
@@ -71,15 +68,39 @@ cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
                               cudaStream_t st);
 
-// ---- a4 (K3): inverse-Cholesky factor append + coefficients (u_new = gamma c*) ----
-cudaError_t launch_factor_append(int32_t k, int64_t B, const int32_t* nstar, const float* cstar, const float* G,
-                                 int64_t ldg, float* F, int64_t ldf, float* u, int64_t ldu, float* X, int64_t ldx,
-                                 int32_t* support, int64_t lds, int32_t* status, cudaStream_t st);
-// ---- a5 (K4): residual gather + norm + eps mask + planes ----
-cudaError_t launch_residual(int32_t k, int32_t S, float eps, int64_t B, const float* Y, int64_t ldy, int64_t M,
-                            int64_t Mp, const float* At, const float* X, int64_t ldx, const int32_t* support,
-                            int64_t lds, float* R32, void* Rb, float* R_hi, float* R_lo, float* resid,
-                            int32_t* n_iter, int32_t* status, cudaStream_t st);
+// ---- a3 + a4 + a5 fused per signal (k_update.cu) ----
+struct UpdateLaunch {
+  int32_t k, S;
+  float eps;
+  int64_t B, N, M, Mp;
+  const float2* part;      // screen partials (tensor-core modes) or nullptr (then nstar/cstar are used)
+  int tiles_n;
+  float window;
+  const int32_t* nstar;
+  const float* cstar;
+  const float* At;
+  const float* inv_norm;
+  const float* G;
+  int64_t ldg;
+  const float* Y;
+  int64_t ldy;
+  float* F;
+  int64_t ldf;             // multiple of 4 (16-byte aligned packed-F rows)
+  float* U;
+  int64_t ldu;
+  float* X;
+  int64_t ldx;
+  int32_t* support;
+  int64_t lds;
+  float* R32;
+  void* Rb;
+  float* Rhi;
+  float* Rlo;
+  float* resid;
+  int32_t* n_iter;
+  int32_t* status;
+};
+cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st);
 cudaError_t launch_densify(const float* X, int64_t ldx, const int32_t* support, int64_t lds,
                            const int32_t* n_iter, int64_t B, int32_t S, int64_t N, float* Xd,
                            int64_t ldxd, cudaStream_t st);
