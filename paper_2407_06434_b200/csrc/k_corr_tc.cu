@@ -95,19 +95,31 @@ __device__ __forceinline__ void mbar_arrive_cta0(uint64_t* bar) {
                : "memory");
 }
 
+// 2-D TMA tile load with an L2 cache policy (A tiles: evict_last, they are re-read by every row block;
+// residual tiles: evict_normal, they are re-read across the N tiles of their raster group)
 template <int CG>
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int k, int row) {
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int k, int row,
+                                            uint64_t policy) {
   if constexpr (CG == 1) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
   } else {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(k), "r"(row), "r"(smem_u32(bar) & 0xFEFFFFFFu), "l"(policy)
         : "memory");
   }
+}
+
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 // K-major, 128-byte-swizzled UMMA shared-memory descriptor (8-row x 128 B atoms, SBO = 1024 B)
@@ -250,6 +262,7 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t keep = l2_policy(true), normal = l2_policy(false);
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         int tm, tn;
         sched.coords(t, tm, tn);
@@ -261,9 +274,9 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
           if (leader) mbar_expect_tx(&full[stage], C_::STAGE_BYTES * CG);
 #pragma unroll
           for (int p = 0; p < K_::NPLANES; ++p) {
-            tma_load_2d<CG>(&maps.r[p], &full[stage], st + p * C_::R_BYTES, kb * K_::BK, row0);
+            tma_load_2d<CG>(&maps.r[p], &full[stage], st + p * C_::R_BYTES, kb * K_::BK, row0, normal);
             tma_load_2d<CG>(&maps.a[p], &full[stage], st + K_::NPLANES * C_::R_BYTES + p * C_::A_BYTES,
-                            kb * K_::BK, atom0);
+                            kb * K_::BK, atom0, keep);
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }

@@ -94,6 +94,33 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// L2 policies: the 64 MB (c4) fp32 atom table is re-read by every signal and should stay in L2;
+// y, the residual planes and the factors are streamed once per iteration.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg_policy(const float4* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_policy(float4* ptr, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+               ::"l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_policy(uint2* ptr, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
+               ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+}
+
 template <int T>
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -142,7 +169,8 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   float* u = z + Sp;
   float* xs = u + Sp;
   int* ss = reinterpret_cast<int*>(xs + Sp);
-  int* cand = ss + Sp;
+  uint32_t* ro = reinterpret_cast<uint32_t*>(ss + Sp);   // atom row offsets (float4 units) for the gather
+  int* cand = reinterpret_cast<int*>(ro + Sp);
   __shared__ float red[T / 32];
   __shared__ Cand red_c[T / 32];
   __shared__ int ncand;
@@ -275,6 +303,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   for (int j = tid; j < k; j += T) {
     const int s = a.support[b * a.lds + j];
     ss[j] = s;
+    ro[j] = (uint32_t)s * (uint32_t)q4;
     dup |= (s == n);
     w[j] = grow[s];                     // [A^T A]_{n*, s_j}
     u[j] = a.U[b * a.ldu + j];
@@ -327,54 +356,65 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
     a.X[b * a.ldx + k] = xk;
     xs[k] = xk;
     ss[k] = n;
+    ro[k] = (uint32_t)n * (uint32_t)q4;
     a.U[b * a.ldu + k] = unew;
     a.support[b * a.lds + k] = n;
   }
   __syncthreads();
 
   // ---- a5: residual r = y - A_S x, ||r||, eps test, next screening operand ------------------------
-  // The gather is L2-bandwidth bound: every thread keeps 4 atoms x CH float4 loads in flight.
+  // L2-bandwidth bound gather: per atom pair, every thread issues its 2 x CH float4 loads before the
+  // FMAs; with T * CH == Mp / 4 (the benchmark shapes) no load is predicated.
   const int kk = k + 1;
+  const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
   float4 acc[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* A4 = reinterpret_cast<const float4*>(a.At);
-  int j = 0;
-  for (; j + 4 <= kk; j += 4) {
-    float4 av[4][CH];
+  const float4* A4 = reinterpret_cast<const float4*>(a.At) + tid;
+  if (T * CH == q4) {
+    int j = 0;
+    for (; j + 2 <= kk; j += 2) {
+      const float4* r0 = A4 + ro[j];
+      const float4* r1 = A4 + ro[j + 1];
+      float4 v0[CH], v1[CH];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float4* row = A4 + (int64_t)ss[j + t] * q4;
+      for (int c = 0; c < CH; ++c) v0[c] = ldg_policy(r0 + c * T, keep);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int q = tid + c * T;
-        av[t][c] = q < q4 ? __ldg(row + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float xj = xs[j + t];
+      for (int c = 0; c < CH; ++c) v1[c] = ldg_policy(r1 + c * T, keep);
+      const float x0 = xs[j], x1 = xs[j + 1];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-        acc[c].x = fmaf(xj, av[t][c].x, acc[c].x);
-        acc[c].y = fmaf(xj, av[t][c].y, acc[c].y);
-        acc[c].z = fmaf(xj, av[t][c].z, acc[c].z);
-        acc[c].w = fmaf(xj, av[t][c].w, acc[c].w);
+        acc[c].x = fmaf(x1, v1[c].x, fmaf(x0, v0[c].x, acc[c].x));
+        acc[c].y = fmaf(x1, v1[c].y, fmaf(x0, v0[c].y, acc[c].y));
+        acc[c].z = fmaf(x1, v1[c].z, fmaf(x0, v0[c].z, acc[c].z));
+        acc[c].w = fmaf(x1, v1[c].w, fmaf(x0, v0[c].w, acc[c].w));
       }
     }
-  }
-  for (; j < kk; ++j) {
-    const float xj = xs[j];
-    const float4* row = A4 + (int64_t)ss[j] * q4;
+    if (j < kk) {
+      const float4* r0 = A4 + ro[j];
+      const float x0 = xs[j];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int q = tid + c * T;
-      if (q < q4) {
-        const float4 av = __ldg(row + q);
-        acc[c].x = fmaf(xj, av.x, acc[c].x);
-        acc[c].y = fmaf(xj, av.y, acc[c].y);
-        acc[c].z = fmaf(xj, av.z, acc[c].z);
-        acc[c].w = fmaf(xj, av.w, acc[c].w);
+      for (int c = 0; c < CH; ++c) {
+        const float4 v = ldg_policy(r0 + c * T, keep);
+        acc[c].x = fmaf(x0, v.x, acc[c].x);
+        acc[c].y = fmaf(x0, v.y, acc[c].y);
+        acc[c].z = fmaf(x0, v.z, acc[c].z);
+        acc[c].w = fmaf(x0, v.w, acc[c].w);
+      }
+    }
+  } else {
+    for (int j = 0; j < kk; ++j) {
+      const float4* r0 = A4 + ro[j];
+      const float x0 = xs[j];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (tid + c * T < q4) {
+          const float4 v = ldg_policy(r0 + c * T, keep);
+          acc[c].x = fmaf(x0, v.x, acc[c].x);
+          acc[c].y = fmaf(x0, v.y, acc[c].y);
+          acc[c].z = fmaf(x0, v.z, acc[c].z);
+          acc[c].w = fmaf(x0, v.w, acc[c].w);
+        }
       }
     }
   }
@@ -388,7 +428,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
       const int64_t m = (int64_t)q << 2;
       float4 yv;
       if (yvec && m + 3 < a.M) {
-        yv = __ldcs(reinterpret_cast<const float4*>(y + m));
+        yv = ldg_policy(reinterpret_cast<const float4*>(y + m), stream);
       } else {
         yv.x = m < a.M ? y[m] : 0.f;
         yv.y = m + 1 < a.M ? y[m + 1] : 0.f;
@@ -397,13 +437,13 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
       }
       const float4 r = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
       part = fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, fmaf(r.w, r.w, part))));
-      if (a.R32) reinterpret_cast<float4*>(a.R32 + b * a.Mp)[q] = r;
+      if (a.R32) stg_policy(reinterpret_cast<float4*>(a.R32 + b * a.Mp) + q, r, stream);
       if (a.Rb) {
         __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&p0);
         pk.y = *reinterpret_cast<uint32_t*>(&p1);
-        reinterpret_cast<uint2*>(a.Rb + b * a.Mp)[q] = pk;
+        stg_policy(reinterpret_cast<uint2*>(a.Rb + b * a.Mp) + q, pk, stream);
       }
       if (a.Rhi) {
         const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
@@ -438,7 +478,9 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, cudaStr
 
 template <bool REFINE>
 static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, cudaStream_t st) {
-  const int64_t q4 = a.Mp / 4;
+  const int64_t q4 = a.Mp / 4;   // float4 chunks per row; T * CH == q4 at powers of two
+  if (q4 <= 32) return launch_t<REFINE, 32, 1>(a, B, smem, st);
+  if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, st);
   if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, st);
   if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, st);
   if (q4 <= 512) return launch_t<REFINE, 128, 4>(a, B, smem, st);
@@ -463,7 +505,7 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.f_stage = (fk * 4 <= (int64_t)64 * 1024 && L.ldf % 4 == 0) ? 1 : 0;
   a.region_floats = (int)((a.f_stage && fk > rowf) ? fk : rowf);
   const int64_t Sp = (L.k + 4) & ~3;
-  const size_t smem = (size_t)a.region_floats * 4 + (size_t)Sp * 5 * 4 + (refine ? RF_CAP * 4 : 0);
+  const size_t smem = (size_t)a.region_floats * 4 + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
   return refine ? launch_r<true>(a, L.B, smem, st) : launch_r<false>(a, L.B, smem, st);
 }
 
