@@ -463,29 +463,46 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
 }
 
 template <bool REFINE, int T, int CH>
-static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, cudaStream_t st) {
+static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   auto kern = k_update<REFINE, T, CH>;
-  // static (~12 KB) + dynamic shared memory may exceed the 48 KB default: opt in once per variant
+  // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   static bool opted = false;
   if (!opted) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return e;
     opted = true;
   }
-  kern<<<(unsigned)B, T, smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)B);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (persist > 0) {
+    // keep the fp32 atom table (re-read by every signal's gather) in the persisting L2 carve-out;
+    // a launch attribute, so the caller's stream is left untouched
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(a.At);
+    attr[0].val.accessPolicyWindow.num_bytes = persist;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <bool REFINE>
-static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, cudaStream_t st) {
+static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   const int64_t q4 = a.Mp / 4;   // float4 chunks per row; T * CH == q4 at powers of two
-  if (q4 <= 32) return launch_t<REFINE, 32, 1>(a, B, smem, st);
-  if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, st);
-  if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, st);
-  if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, st);
-  if (q4 <= 512) return launch_t<REFINE, 128, 4>(a, B, smem, st);
-  if (q4 <= 1024) return launch_t<REFINE, 256, 4>(a, B, smem, st);
-  if (q4 <= 2048) return launch_t<REFINE, 256, 8>(a, B, smem, st);
+  if (q4 <= 32) return launch_t<REFINE, 32, 1>(a, B, smem, persist, st);
+  if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, persist, st);
+  if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, persist, st);
+  if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, persist, st);
+  if (q4 <= 512) return launch_t<REFINE, 128, 4>(a, B, smem, persist, st);
+  if (q4 <= 1024) return launch_t<REFINE, 256, 4>(a, B, smem, persist, st);
+  if (q4 <= 2048) return launch_t<REFINE, 256, 8>(a, B, smem, persist, st);
   return cudaErrorNotSupported;   // M > 8192
 }
 
@@ -506,7 +523,8 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.region_floats = (int)((a.f_stage && fk > rowf) ? fk : rowf);
   const int64_t Sp = (L.k + 4) & ~3;
   const size_t smem = (size_t)a.region_floats * 4 + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
-  return refine ? launch_r<true>(a, L.B, smem, st) : launch_r<false>(a, L.B, smem, st);
+  return refine ? launch_r<true>(a, L.B, smem, L.l2_persist_bytes, st)
+                : launch_r<false>(a, L.B, smem, L.l2_persist_bytes, st);
 }
 
 }  // namespace ompb

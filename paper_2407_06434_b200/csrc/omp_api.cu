@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <climits>
@@ -31,6 +32,7 @@ struct ompHandle_st {
   int64_t M = 0, N = 0, Mp = 0, Np = 0;
   int mode = OMP_CORR_3XTF32;
   float window = 0.f;      // screening window / ||r|| (tensor-core modes), DESIGN.md §5
+  size_t l2_persist = 0;   // bytes of At under a persisting L2 access-policy window (0: off)
   // dictionary (owned): FP32 copy of A^T (Np x Mp), the screen's plane(s), 1/||a_n||, Gram
   float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *inv_norm = nullptr, *G = nullptr;
   uint16_t* Ab = nullptr;  // bf16 plane
@@ -232,6 +234,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     U.support = support; U.lds = lds;
     U.R32 = h->R32; U.Rb = h->Rb; U.Rhi = h->R_hi; U.Rlo = h->R_lo;
     U.resid = resid; U.n_iter = n_iter; U.status = status;
+    U.l2_persist_bytes = h->l2_persist;
     L.begin(3);
     e = launch_update(U, st);
     L.end(3);
@@ -321,6 +324,23 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   h->Np = round_up(N, N_TILE);
   h->mode = corr_mode;
   h->window = screening_window(corr_mode, h->Mp);
+  {
+    // persisting-L2 carve-out for the fp32 atom table gathered by every signal (K4); only ever
+    // raises the device limit; OMP_B200_L2_PERSIST=0 disables it
+    const char* env = getenv("OMP_B200_L2_PERSIST");
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+    const size_t want = (size_t)h->Np * h->Mp * sizeof(float);
+    if (!(env && env[0] == '0') && maxp > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      const size_t lim = want < (size_t)maxp ? want : (size_t)maxp;
+      if (cur < lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      h->l2_persist = cur < want ? cur : want;
+    }
+    cudaGetLastError();
+  }
   const size_t plane = (size_t)h->Np * h->Mp;
   bool ok = dalloc(h->At, plane) && dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
             dalloc(h->dflags, 2);

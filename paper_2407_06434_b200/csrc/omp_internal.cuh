@@ -99,6 +99,7 @@ struct UpdateLaunch {
   float* resid;
   int32_t* n_iter;
   int32_t* status;
+  size_t l2_persist_bytes;  // > 0: launch with a persisting L2 access-policy window over At
 };
 cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st);
 cudaError_t launch_densify(const float* X, int64_t ldx, const int32_t* support, int64_t lds,
