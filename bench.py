@@ -128,20 +128,29 @@ def ncu_traffic(kernel_key: str, config_name: str):
 
 
 # ------------------------------------------------------------------------------ roofline model
-def kernel_work(cfg, B):
-    """Algorithmic work per launch (per signal-iteration x the signals one launch covers)."""
+def kernel_work(cfg, B, mode):
+    """Algorithmic work per launch (SURVEY §8(d) per signal-iteration, x the B signals one launch covers,
+    at the mean support size k = (S-1)/2 of a full run).  DESIGN.md §6 states each figure."""
     M, N, S = cfg["M"], cfg["N"], cfg["S"]
-    k_avg = (S - 1) / 2.0
+    Mp = -(-M // 64) * 64
+    k = (S - 1) / 2.0
+    tiles = math.ceil(N / 256)
+    planes = {"bf16": 2.0, "3xtf32": 8.0, "simt": 0.0}[mode]
+    # update = exact selection + factor append + residual, split into streamed (HBM) and gathered (L2)
+    hbm = B * (4.0 * Mp                      # fp32 residual row read by the selection
+               + 8.0 * 4 * tiles             # screen partials
+               + 4.0 * k * (k + 1) / 2       # packed F_k staged once
+               + 4.0 * (k + 2) * 3           # new F column, x, u
+               + 4.0 * M                     # y
+               + (4.0 + planes) * Mp)        # residual written: fp32 + screen planes
+    l2 = B * 4.0 * Mp * (k + 1 + 1)          # (k+1) gathered atom rows + ~1 candidate row
     return {
-        # screen GEMM: 2 M N flops per signal-iteration (the FP32-equivalent contraction)
-        "correlation": ("tensor", 2.0 * M * N * B, "TFLOP/s"),
-        # refine: the fp32 residual row + ~2 candidate atom rows + partials
-        "select": ("hbm", B * (4.0 * M + 2 * 4.0 * M + 8.0 * 4 * math.ceil(N / 256)), "GB/s"),
-        # factor append: packed F read twice, new column write, Gram gathers
-        "factor_append": ("hbm", B * (2 * 4.0 * k_avg * (k_avg + 1) / 2 + 4.0 * (k_avg + 2) + 32.0 * k_avg), "GB/s"),
-        # residual: y read, fp32 + bf16 planes written, (k+1) atom rows gathered (L2)
-        "residual": ("hbm", B * (4.0 * M + 6.0 * M + 4.0 * (k_avg + 1) * M), "GB/s"),
-        "init": ("hbm", B * (4.0 * M + 6.0 * M), "GB/s"),
+        # screen GEMM: 2 M N flops per signal-iteration (the contraction C = A^T R)
+        "correlation": ("tensor", 2.0 * M * N * B, "TFLOP/s", None),
+        # standalone argmax over the FP32 C (SIMT mode): 4N bytes per signal
+        "select": ("hbm", B * 4.0 * N, "GB/s", None),
+        "update": ("hbm", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
+        "init": ("hbm", B * (4.0 * M + (4.0 + planes) * Mp), "GB/s", None),
     }
 
 
@@ -248,9 +257,9 @@ def main():
                "d2h_bytes_per_step": int(sum(o.nbytes for o in outs)) * world}
 
     # roofline of the dominant kernel (events measured live over the timed steps, this rank)
-    work = kernel_work(cfg, B)
+    work = kernel_work(cfg, B, args.mode)
     dom = max((k for k in kern if k in work), key=lambda k: kern[k][0])
-    bound, per_launch, unit = work[dom]
+    bound, per_launch, unit, split = work[dom]
     t_launch = kern[dom][0] / max(1, kern[dom][1]) / 1e3
     peaks = measured_peaks()
     if bound == "tensor":
@@ -270,6 +279,22 @@ def main():
     roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": achieved / peak, "traffic": ncu_traffic(dom, args.config), "peak_source": peak_src,
                 "work_per_launch": per_launch, "launch_ms": t_launch * 1e3}
+    if split:
+        # the update kernel's atom gather is served by L2: report the effective-bandwidth split and the
+        # L2 roofline (L2 peak from ncu: lts throughput % on the r01 capture)
+        l2_peak = 25600.0
+        roofline.update({"hbm_bytes": split["hbm_bytes"], "l2_gather_bytes": split["l2_gather_bytes"],
+                         "effective": "achieved = (streamed HBM bytes + L2 gather bytes) / launch time",
+                         "l2_peak_gbs": l2_peak, "frac_of_l2_peak": achieved / l2_peak})
+    other = {k: kern[k] for k in kern if k in work and k != dom and kern[k][1] > 0}
+    roofline["others"] = {}
+    for k, (tot_ms, n_l) in other.items():
+        b2, w2, u2, _ = work[k]
+        t2 = tot_ms / n_l / 1e3
+        if b2 == "tensor":
+            roofline["others"][k] = {"achieved_tflops": w2 / t2 / 1e12, "launch_ms": t2 * 1e3}
+        else:
+            roofline["others"][k] = {"achieved_gbs": w2 / t2 / 1e9, "launch_ms": t2 * 1e3}
     kernels = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / max(1e-9, sum(x[0] for x in kern.values()))}
                for k, v in kern.items()}
 

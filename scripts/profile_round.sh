@@ -10,7 +10,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 echo "launch list rc=$?"
 # 2) one full capture of each hot kernel at iteration 64 (k = 64 = mean support size at c4)
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"k1_corr_tc|k4_residual|k3_factor|k2_refine" -s 256 -c 4 -o $OUT/prof_${TAG} -f \
+  -k regex:"k1_corr_tc|k_update" -s 128 -c 2 -o $OUT/prof_${TAG} -f \
   python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline "$@" > $OUT/prof_${TAG}.bench.json 2> $OUT/prof_${TAG}.err
 echo "full capture rc=$?"
 ls -la $OUT

@@ -13,7 +13,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = {"k1_corr_tc": "correlation", "k1_corr_simt": "correlation", "k2_refine": "select", "k2_select": "select",
-        "k3_factor": "factor_append", "k4_residual": "residual", "k_batch_init": "init"}
+        "k3_factor": "factor_append", "k4_residual": "residual", "k_batch_init": "init", "k_update": "update"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
