@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--oracle-sample", type=int, default=None, help="signals in the CPU oracle sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for single-GPU testing")
     return p.parse_args()
 
 
@@ -166,10 +167,13 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     cfg = config(args.config)
     B_total = args.batch or cfg["B"]
     per = -(-B_total // world)
@@ -179,9 +183,11 @@ def main():
 
     # dictionary: generated on rank 0, broadcast once over NCCL (north star); signals: own shard
     A_np = make_dictionary(M, N, cfg["seed"])
-    A = torch.from_numpy(A_np).to(dev) if rank == 0 else torch.empty((M, N), dtype=torch.float32, device=dev)
+    comm = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    A = torch.from_numpy(A_np).to(comm) if rank == 0 else torch.empty((M, N), dtype=torch.float32, device=comm)
     if world > 1:
-        dist.broadcast(A, src=0)
+        dist.broadcast(A, src=0)          # once per dictionary, over NVLink with NCCL
+    A = A.to(dev)
     Y_np = make_signals(A.cpu().numpy(), range(lo, hi), cfg["seed"], cfg["sparsity"], cfg["sigma"], device=dev)
     Y = torch.from_numpy(Y_np).to(dev)
     eps32 = None if eps is None else float(np.float32(eps))
@@ -196,7 +202,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=comm)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -208,7 +214,8 @@ def main():
     # timed region: per-kernel CUDA events inside the library (profiling mode) + step events
     h.profile(True)
     h.profile_read(reset=True)
-    clocks = ClockSampler(local)
+    props = torch.cuda.get_device_properties(dev)
+    clocks = ClockSampler(f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:{props.pci_device_id:02X}.0")
     clocks.start()
     step_ms = []
     launches = 0
