@@ -30,7 +30,8 @@ namespace tc {
 constexpr int BM = 128;       // signal rows per CTA (UMMA M per CTA)
 constexpr int BN = 256;       // atoms per tile (UMMA N)
 constexpr int GM = 16;        // row-blocks per raster group
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_THREADS = 256;   // warps 4..11: two warps per TMEM lane group, 128 columns each
+constexpr int NUM_THREADS = 128 + EPI_THREADS;
 constexpr int MODE_STORE = 0, MODE_TOPK = 1;
 
 // Operand kinds.  Every stage holds one 128-byte-wide K slab of each plane.
@@ -200,8 +201,8 @@ struct EpiArgs {
   float* C;                 // MODE_STORE
   int64_t ldc;
   int64_t ncols;            // columns < ncols are stored
-  const float* inv_norm;    // MODE_TOPK
-  float2* part;             // MODE_TOPK: rows x tiles_n x TOPK {value, index bits}
+  const float* norm;        // MODE_STORE: ||a_n|| (the screen runs on normalised atoms)
+  float2* part;             // MODE_TOPK: rows x (2 tiles_n) x TOPK {value, index bits}
   const int32_t* status;    // MODE_TOPK: finished rows are skipped (may be null)
   const float* resid;       // MODE_TOPK: ||r_b|| of the residual being screened
   float window;             // MODE_TOPK: screening window / ||r||
@@ -239,7 +240,7 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128 * CG);
+      mbar_init(&tempty[a], EPI_THREADS * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -321,7 +322,10 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global =====================
-    const int ew = warp - 4;
+    // Eight warps: warp w reads TMEM lane group (w % 4) (hardware rule: warp i owns lanes
+    // 32 (i % 4) .. +31) and the column half (w - 4) / 4, i.e. 128 atoms of the 256-atom tile.
+    const int ew = warp - 4, lg = ew & 3, half = ew >> 2;
+    constexpr int HB = BN / 2;
     int it = 0;
     for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
       int tm, tn;
@@ -330,61 +334,50 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[a], aphase);
       fence_after();
-      const int row = tm * BM * CG + (int)rank * BM + ew * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(a * BN);
+      const int row = tm * BM * CG + (int)rank * BM + lg * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * BN + half * HB);
+      const int64_t colh = (int64_t)tn * BN + half * HB;
       bool live = row < rows;
       if constexpr (MODE == MODE_STORE) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < HB / 32; ++c) {
           float v[32];
           tmem_ld32(taddr + (uint32_t)(c * 32), v);
-          const int64_t col0 = (int64_t)tn * BN + c * 32;
+          const int64_t col0 = colh + c * 32;
           if (live) {
             float* dst = ep.C + (int64_t)row * ep.ldc + col0;
-            if (col0 + 32 <= ep.ncols && (ep.ldc & 3) == 0) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q)
-                reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < 32; ++q)
-                if (col0 + q < ep.ncols) dst[q] = v[q];
-            }
+            for (int q = 0; q < 32; ++q)      // undo the normalisation: C = A^T R
+              if (col0 + q < ep.ncols) dst[q] = v[q] * __ldg(ep.norm + col0 + q);
           }
         }
       } else {
-        // The refine kernel needs every atom within W = window ||r_b|| of the GLOBAL max; since the
-        // global max >= this tile's max, the entries within W of the tile max are a superset.
-        // Pass A: normalised chunk maxima (FMUL + FMNMX + FADD per value; the FADD sum is NaN iff
-        // some value is NaN, every term being >= 0).  Pass B: re-read only the chunks reaching
-        // tile_max - W and keep the top TOPK of those entries, in index order on ties.
+        // The exact selection needs every atom within W = window ||r_b|| of the GLOBAL maximum of
+        // |c~_n| (the screen runs on normalised atoms, so c~ is already |<r, a_n>| / ||a_n||); the
+        // global maximum is >= this half tile's, so the entries within W of the half-tile maximum
+        // are a superset.  Pass A: chunk maxima (one FMNMX per value).  Pass B: re-read the chunks
+        // reaching max - W and emit their in-window entries in index order (predicated stores; at
+        // most TOPK, an overflow is flagged in the last slot with the half-tile maximum).
         float W = 0.f;
         if (live && ep.status) live = ep.status[row] == SIG_RUNNING;
         if (live) W = ep.window * ep.resid[row];
-        const float* wn = ep.inv_norm + (int64_t)tn * BN;
-        float cm[BN / 32];
-        float tmax = 0.f, csum = 0.f;
+        float cm[HB / 32];
+        float tmax = 0.f;
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < HB / 32; ++c) {
           float v[32];
           tmem_ld32(taddr + (uint32_t)(c * 32), v);
           float m = 0.f;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float s = fabsf(v[q]) * __ldg(wn + c * 32 + q);
-            m = fmaxf(m, s);
-            csum += s;
-          }
+          for (int q = 0; q < 32; ++q) m = fmaxf(m, fabsf(v[q]));
           cm[c] = m;
           tmax = fmaxf(tmax, m);
         }
         const float thr = tmax - W;
-        float bv[TOPK];
-        int bi[TOPK];
+        float2* dst = ep.part + ((int64_t)row * (2 * tiles_n) + 2 * tn + half) * TOPK;
+        int cnt = 0;
 #pragma unroll
-        for (int j = 0; j < TOPK; ++j) { bv[j] = -1.f; bi[j] = -1; }
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < HB / 32; ++c) {
           const bool need = live && cm[c] >= thr;
           if (!__any_sync(0xffffffffu, need)) continue;       // warp-uniform: tcgen05.ld is .aligned
           float v[32];
@@ -392,28 +385,17 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
           if (need) {
 #pragma unroll
             for (int q = 0; q < 32; ++q) {
-              float cv = fabsf(v[q]) * __ldg(wn + c * 32 + q);
-              if (cv >= thr && cv > bv[TOPK - 1]) {
-                int ci = tn * BN + c * 32 + q;
-#pragma unroll
-                for (int j = 0; j < TOPK; ++j) {
-                  if (cv > bv[j]) {
-                    const float tv = bv[j];
-                    const int ti = bi[j];
-                    bv[j] = cv; bi[j] = ci;
-                    cv = tv; ci = ti;
-                  }
-                }
+              const float s = fabsf(v[q]);
+              if (s >= thr) {
+                if (cnt < TOPK) dst[cnt] = make_float2(s, __int_as_float((int)colh + c * 32 + q));
+                ++cnt;
               }
             }
           }
         }
         if (live) {
-          if (isnan(csum)) bi[0] = SEL_NAN;
-          float4* dst = reinterpret_cast<float4*>(ep.part + ((int64_t)row * tiles_n + tn) * TOPK);
-#pragma unroll
-          for (int j = 0; j < TOPK; j += 2)
-            dst[j / 2] = make_float4(bv[j], __int_as_float(bi[j]), bv[j + 1], __int_as_float(bi[j + 1]));
+          for (int j = cnt; j < TOPK; ++j) dst[j] = make_float2(-1.f, __int_as_float(-1));
+          if (cnt > TOPK) dst[TOPK - 1] = make_float2(tmax, __int_as_float(SEL_OVERFLOW));
         }
       }
       fence_before();
@@ -532,15 +514,14 @@ static cudaError_t dispatch(int kind, const Operand& R, const Operand& At, int64
 }  // namespace tc
 
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
-                           int64_t ncols, cudaStream_t st) {
-  tc::EpiArgs ep{C, ldc, ncols, nullptr, nullptr, nullptr, nullptr, 0.f};
+                           int64_t ncols, const float* norm, cudaStream_t st) {
+  tc::EpiArgs ep{C, ldc, ncols, norm, nullptr, nullptr, nullptr, 0.f};
   return tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
 }
 
-cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const float* inv_norm,
-                                const int32_t* status, const float* resid, float window, float2* part,
-                                cudaStream_t st) {
-  tc::EpiArgs ep{nullptr, 0, At.rows, inv_norm, part, status, resid, window};
+cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* status,
+                                const float* resid, float window, float2* part, cudaStream_t st) {
+  tc::EpiArgs ep{nullptr, 0, At.rows, nullptr, part, status, resid, window};
   return tc::dispatch<tc::MODE_TOPK>(kind, R, At, K, ep, st);
 }
 

@@ -43,43 +43,48 @@ __device__ __forceinline__ double block_sum_double(double v, double* red) {
   return red[0];
 }
 
-// One CTA per (padded) atom n: copy a_n into row n of the planes and compute ||a_n|| in FP64
-// (PAPER.md:46 denominator; App. A).
+// One CTA per (padded) atom n: ||a_n|| in FP64 (PAPER.md:46 denominator; App. A), then
+// row n of the FP32 copy (raw a_n, used by the exact re-evaluation, the gather and the Gram matrix)
+// and of the screen planes of the NORMALISED atom a_n / ||a_n|| (the screen's correlations are then
+// already the normalised |<r, a_n>| / ||a_n|| of PAPER.md:46, App. A "invariant to column norm").
 __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t N, int64_t lda, int64_t Mp,
                                  float* __restrict__ At, __nv_bfloat16* __restrict__ Ab, float* __restrict__ Ahi,
-                                 float* __restrict__ Alo, float* __restrict__ inv_norm, int* bad_zero,
-                                 int* bad_nonfinite) {
+                                 float* __restrict__ Alo, float* __restrict__ norm, float* __restrict__ inv_norm,
+                                 int* bad_zero, int* bad_nonfinite) {
   __shared__ double red[32];
   const int64_t n = blockIdx.x;
   double ss = 0.0;
   bool finite = true;
-  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
-    float v = 0.f;
-    if (n < N && m < M) {
-      v = A[n * lda + m];
+  if (n < N)
+    for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+      const float v = A[n * lda + m];
       finite &= isfinite(v);
       ss += (double)v * (double)v;
     }
-    put_planes(n * Mp + m, v, At, Ab, Ahi, Alo);
-  }
   const int any_bad = __syncthreads_or(!finite);
   ss = block_sum_double(ss, red);
+  const bool ok = n < N && ss > 0.0 && !any_bad;
+  const float inv = ok ? (float)(1.0 / sqrt(ss)) : 0.f;
+  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
+    const float v = (n < N && m < M) ? A[n * lda + m] : 0.f;
+    At[n * Mp + m] = v;
+    put_planes(n * Mp + m, v * inv, nullptr, Ab, Ahi, Alo);
+  }
   if (threadIdx.x == 0) {
     if (n < N) {
       if (any_bad) atomicMin(bad_nonfinite, (int)n);
       else if (ss == 0.0) atomicMin(bad_zero, (int)n);
-      inv_norm[n] = (ss > 0.0 && !any_bad) ? (float)(1.0 / sqrt(ss)) : 0.f;
-    } else {
-      inv_norm[n] = 0.f;   // padded atoms never win the argmax
     }
+    inv_norm[n] = inv;                 // padded atoms: 0, they never win the argmax
+    norm[n] = ok ? (float)sqrt(ss) : 0.f;
   }
 }
 
 cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
-                                 float* At, void* At_bf16, float* At_hi, float* At_lo, float* inv_norm,
-                                 int* bad_zero, int* bad_nonfinite, cudaStream_t st) {
+                                 float* At, void* At_bf16, float* At_hi, float* At_lo, float* norm,
+                                 float* inv_norm, int* bad_zero, int* bad_nonfinite, cudaStream_t st) {
   k0_prepare_atoms<<<(unsigned)Np, 128, 0, st>>>(A, M, N, lda, Mp, At, (__nv_bfloat16*)At_bf16, At_hi, At_lo,
-                                                 inv_norm, bad_zero, bad_nonfinite);
+                                                 norm, inv_norm, bad_zero, bad_nonfinite);
   return cudaGetLastError();
 }
 

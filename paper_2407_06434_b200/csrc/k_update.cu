@@ -5,9 +5,9 @@
 //      The screen (k_corr_tc.cu) bounds |c~_n - c_n| <= c0 ||a_n|| ||r_b||, i.e. c0 ||r_b|| in
 //      normalised units for every n, so the exact argmax lies in
 //        { n : v~_n >= max v~ - window ||r_b|| },  window = 2 (c0 + c0')   (c0' bounds this FP32 dot).
-//      The screen kept, per 256-atom tile, the top-4 entries within the window of the tile max; a
-//      tile whose 4th kept entry is still inside the global window is re-evaluated in full, an
-//      overfull candidate list falls back to all N atoms.  Every candidate is re-evaluated as an
+//      The screen kept, per 128-atom group, its entries within the window of the group max (up to 4,
+//      in index order; more are flagged as an overflow, and such a group is re-evaluated in full when
+//      its maximum is inside the global window); an overfull candidate list falls back to all N atoms.  Every candidate is re-evaluated as an
 //      FP32 dot of the fp32 residual and the fp32 atom in a fixed order.  (REFINE = false: n*, c*
 //      come from the standalone argmax over a materialised FP32 C, k_select.cu.)
 //
@@ -43,7 +43,7 @@ struct UpdateArgs {
   int64_t N, M, Mp;
   // selection inputs
   const float2* part;   // screen partials (REFINE)
-  int tiles_n;
+  int groups;           // screen partial groups per row (Np / SCREEN_GROUP)
   float window;
   const int32_t* nstar; // preselected (SIMT mode)
   const float* cstar;
@@ -193,20 +193,20 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
     const float rn = a.resid[b];
-    const float2* P = a.part + b * (int64_t)a.tiles_n * TOPK;
-    const int E = a.tiles_n * TOPK;
+    const float2* P = a.part + b * (int64_t)a.groups * TOPK;
+    const int E = a.groups * TOPK;
     float vmax = -1.f;
-    bool nan_seen = false;
-    for (int e = tid; e < E; e += T) {
-      const float2 p = P[e];
-      nan_seen |= (__float_as_int(p.y) == SEL_NAN) | isnan(p.x);
-      vmax = fmaxf(vmax, p.x);
-    }
+    for (int e = tid; e < E; e += T) vmax = fmaxf(vmax, P[e].x);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     if (lane == 0) red[warp] = vmax;
-    const int any_nan = __syncthreads_or(nan_seen || !isfinite(rn));
-    if (any_nan) {
+    __syncthreads();
+    vmax = red[0];
+#pragma unroll
+    for (int i = 1; i < T / 32; ++i) vmax = fmaxf(vmax, red[i]);
+    // every finite, nonzero residual leaves >= 1 entry per group (the group maximum itself); no entry
+    // at all means the screened correlations were NaN
+    if (!(vmax >= 0.f) || !isfinite(rn)) {
       if (tid == 0) a.status[b] = OMP_SIG_NAN;
       return;
     }
@@ -214,15 +214,14 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
       if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
       return;
     }
-    vmax = red[0];
-#pragma unroll
-    for (int i = 1; i < T / 32; ++i) vmax = fmaxf(vmax, red[i]);
     const float thr = vmax - a.window * rn;
     bool full = false;
-    for (int t = tid; t < a.tiles_n; t += T) {
-      if (P[t * TOPK + TOPK - 1].x >= thr) {            // tile may hold more candidates: all of it
-        const int n0 = t * N_TILE;
-        const int cnt = (int)min((int64_t)N_TILE, a.N - n0);
+    for (int t = tid; t < a.groups; t += T) {
+      const float2 last = P[t * TOPK + TOPK - 1];
+      const int nl = __float_as_int(last.y);
+      if (nl == SEL_OVERFLOW && last.x >= thr) {         // more in-window entries than kept: all of it
+        const int n0 = t * SCREEN_GROUP;
+        const int cnt = (int)min((int64_t)SCREEN_GROUP, a.N - n0);
         if (cnt > 0) {
           const int at = atomicAdd(&ncand, cnt);
           if (at + cnt > RF_CAP) full = true;
@@ -245,22 +244,24 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
     for (int q = tid; q < q4; q += T) rsm[q] = r4g[q];
     full = __syncthreads_or(full);
     Cand best{-1.f, 0x7fffffff, 0.f};
+    bool nan_c = false;
     const int count = full ? (int)a.N : min(ncand, RF_CAP);
     for (int j = warp; j < count; j += T / 32) {
       const int n = full ? j : cand[j];
       const float c = warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane);
+      nan_c |= isnan(c);
       const Cand cd{fabsf(c) * a.inv_norm[n], n, c};
       if (cand_better(cd, best)) best = cd;
     }
     if (lane == 0) red_c[warp] = best;
-    __syncthreads();                                    // residual row no longer needed past here
+    const int any_nan = __syncthreads_or(nan_c);      // residual row no longer needed past here
     if (tid == 0) {
       Cand r = red_c[0];
 #pragma unroll
       for (int i = 1; i < T / 32; ++i)
         if (cand_better(red_c[i], r)) r = red_c[i];
       const bool ok = r.w > 0.f && r.n < a.N;
-      sel_n = ok ? r.n : SEL_DEGENERATE;
+      sel_n = any_nan ? SEL_NAN : (ok ? r.n : SEL_DEGENERATE);
       sel_c = ok ? r.c : 0.f;
     }
   } else {
@@ -510,7 +511,7 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
   UpdateArgs a;
   a.k = L.k; a.S = L.S; a.eps = L.eps; a.N = L.N; a.M = L.M; a.Mp = L.Mp;
-  a.part = L.part; a.tiles_n = L.tiles_n; a.window = L.window; a.nstar = L.nstar; a.cstar = L.cstar;
+  a.part = L.part; a.groups = L.groups; a.window = L.window; a.nstar = L.nstar; a.cstar = L.cstar;
   a.At = L.At; a.inv_norm = L.inv_norm; a.G = L.G; a.ldg = L.ldg;
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
   a.support = L.support; a.lds = L.lds; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb; a.Rhi = L.Rhi;

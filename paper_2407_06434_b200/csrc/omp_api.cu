@@ -1,13 +1,15 @@
 // Host orchestrator + C ABI (include/omp_b200.h).
 //
 // One ompBatch = batch init (a1) followed by S iterations of
-//   K1 correlation (a2) -> K2 select (a3) -> K3 factor append (a4) -> K4 residual (a5)
+//   correlation (a2) -> [standalone argmax, SIMT mode] -> update = selection (a3) + factor append (a4)
+//   + residual (a5)
 // all stream-ordered on the caller's stream with no host synchronisation inside the loop
-// (SURVEY §3 "Ours", stack 2).  Finished signals keep their captured result and skip
-// K2-K4 (capture-and-continue).
-// Tensor-core modes: K1 is a screening GEMM (bf16 or 3xTF32 on tcgen05) whose epilogue keeps
-// top-4 candidates per 256-atom tile, and K2 re-evaluates every candidate inside the rigorous
-// screening window in exact FP32 (k_refine.cu).  SIMT mode: FP32 GEMM -> C -> argmax.
+// (SURVEY §3 "Ours", stack 2).  Finished signals keep their captured result and return at the top
+// of the update kernel (capture-and-continue).
+// Tensor-core modes: the correlation is a screening GEMM (bf16 or 3xTF32 on tcgen05, normalised
+// atoms) whose epilogue keeps the in-window entries per 128-atom group, and the update kernel
+// re-evaluates every candidate inside the rigorous screening window in exact FP32.
+// SIMT mode: FP32 GEMM -> C -> argmax.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -34,7 +36,7 @@ struct ompHandle_st {
   float window = 0.f;      // screening window / ||r|| (tensor-core modes), DESIGN.md §5
   size_t l2_persist = 0;   // bytes of At under a persisting L2 access-policy window (0: off)
   // dictionary (owned): FP32 copy of A^T (Np x Mp), the screen's plane(s), 1/||a_n||, Gram
-  float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *inv_norm = nullptr, *G = nullptr;
+  float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *norm = nullptr, *inv_norm = nullptr, *G = nullptr;
   uint16_t* Ab = nullptr;  // bf16 plane
   int* dflags = nullptr;
   // batch workspace
@@ -44,7 +46,7 @@ struct ompHandle_st {
   uint16_t* Rb = nullptr;  // bf16 plane of the residuals
   int32_t* nstar = nullptr;
   float* cstar = nullptr;
-  float2* part = nullptr;   // screening epilogue: (B) x (Np / 256) x TOPK candidates
+  float2* part = nullptr;   // screening epilogue: (B) x (Np / 128) x TOPK candidates
   int64_t capC = 0;         // rows of C (SIMT mode / ompCorrelate)
   int64_t ldf = 0, ldu = 0;
   int64_t lastB = 0;
@@ -169,7 +171,7 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
             dalloc(h->U, (size_t)nB * nS) && dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB);
   if (ok && bf) ok = dalloc(h->Rb, (size_t)nB * h->Mp);
   if (ok && x3) ok = dalloc(h->R_hi, (size_t)nB * h->Mp) && dalloc(h->R_lo, (size_t)nB * h->Mp);
-  if (ok && tc) ok = dalloc(h->part, (size_t)nB * (h->Np / N_TILE) * TOPK);
+  if (ok && tc) ok = dalloc(h->part, (size_t)nB * (h->Np / SCREEN_GROUP) * TOPK);
   if (ok && !tc) ok = dalloc(h->C, (size_t)nB * h->Np);
   h->capC = (ok && !tc) ? nB : 0;
   if (!ok) {
@@ -206,7 +208,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
       // a2: tensor-core screen C~ = A^T R_k; the epilogue keeps per 256-atom tile the top-4 entries
       // within the screening window of the tile maximum
       L.begin(1);
-      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->inv_norm, status, resid, h->window, h->part, st);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, status, resid, h->window, h->part, st);
       L.end(1);
       if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
       if (e != cudaSuccess) return cuda_fail(h, e);
@@ -226,7 +228,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     UpdateLaunch U;
     U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
     U.part = tc_mode(h) ? h->part : nullptr;
-    U.tiles_n = (int)(h->Np / N_TILE);
+    U.groups = (int)(h->Np / SCREEN_GROUP);
     U.window = h->window;
     U.nstar = h->nstar; U.cstar = h->cstar;
     U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
@@ -285,7 +287,7 @@ ompStatus_t ompDestroy(ompHandle_t h) {
   {
     DevGuard g(h->device);
     cudaDeviceSynchronize();
-    dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->inv_norm); dfree(h->G);
+    dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->norm); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
     dfree(h->nstar); dfree(h->cstar); dfree(h->part);
@@ -342,7 +344,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
     cudaGetLastError();
   }
   const size_t plane = (size_t)h->Np * h->Mp;
-  bool ok = dalloc(h->At, plane) && dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
+  bool ok = dalloc(h->At, plane) && dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
             dalloc(h->dflags, 2);
   if (ok && corr_mode == OMP_CORR_BF16) ok = dalloc(h->Ab, plane);
   if (ok && corr_mode == OMP_CORR_3XTF32) ok = dalloc(h->At_hi, plane) && dalloc(h->At_lo, plane);
@@ -354,7 +356,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   int init_flags[2] = {INT_MAX, INT_MAX};
   cudaError_t e = cudaMemcpyAsync(h->dflags, init_flags, sizeof(init_flags), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
-    e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->Ab, h->At_hi, h->At_lo, h->inv_norm,
+    e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->Ab, h->At_hi, h->At_lo, h->norm, h->inv_norm,
                              h->dflags, h->dflags + 1, st);
   int flags[2] = {INT_MAX, INT_MAX};
   if (e == cudaSuccess) e = cudaMemcpyAsync(flags, h->dflags, sizeof(flags), cudaMemcpyDeviceToHost, st);
@@ -464,7 +466,7 @@ ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, 
   cudaError_t e = launch_make_planes(R, B, ldr, h->M, h->Mp, h->R32, h->Rb, h->R_hi, h->R_lo, st);
   const Operand Rop = resid_operand(h, B), At = atoms_operand(h);
   if (e == cudaSuccess)
-    e = tc_mode(h) ? launch_corr_tc(tc_kind(h), Rop, At, h->Mp, h->C, h->Np, h->Np, st)
+    e = tc_mode(h) ? launch_corr_tc(tc_kind(h), Rop, At, h->Mp, h->C, h->Np, h->Np, h->norm, st)
                    : launch_corr_simt(Rop, At, h->Mp, h->C, h->Np, h->Np, st);
   if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
   if (e == cudaSuccess)

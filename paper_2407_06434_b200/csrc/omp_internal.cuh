@@ -14,13 +14,15 @@ constexpr int32_t SIG_RUNNING = -1;
 // selection codes besides an atom index
 constexpr int32_t SEL_DEGENERATE = -1;   // maximum correlation is 0 (exhausted residual)
 constexpr int32_t SEL_NAN = -2;          // a correlation was not finite
+constexpr int32_t SEL_OVERFLOW = -3;     // screen partial: more in-window entries than TOPK slots
 // factor-append pivot threshold: ||a||^2 - ||z||^2 <= TAU_F * ||a||^2 -> DEGENERATE
 constexpr float TAU_F = 1e-5f;
 
 constexpr int K_TILE = 64;     // K padding of every plane (a 128-byte bf16 TMA/UMMA row)
 constexpr int N_TILE = 256;    // atom padding (UMMA N of the correlation kernel)
 constexpr int MAX_S = 512;
-constexpr int TOPK = 4;        // screening candidates kept per (signal, 256-atom tile)
+constexpr int TOPK = 4;        // screening candidates kept per (signal, 128-atom half tile)
+constexpr int SCREEN_GROUP = 128;   // atoms per screen partial (half of the 256-atom UMMA tile)
 
 // screening-GEMM operand kinds
 constexpr int KIND_BF16 = 0;
@@ -41,24 +43,24 @@ struct Operand {
 // FP32 SIMT GEMM (round-to-nearest, sequential K): C written for rows < R.rows, n < ncols
 cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                              int64_t ncols, cudaStream_t st);
-// tcgen05 screening GEMM, C~ stored (diagnostics / numerics tests)
+// tcgen05 screening GEMM on normalised atoms; C~ stored times ||a_n|| (diagnostics / numerics tests)
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
-                           int64_t ncols, cudaStream_t st);
-// tcgen05 screening GEMM, epilogue -> per (row, 256-atom tile) the top-TOPK (|c~| / ||a||, n) among
-// the entries within window * resid[row] of the tile's maximum
-cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const float* inv_norm,
-                                const int32_t* status, const float* resid, float window, float2* part,
-                                cudaStream_t st);
+                           int64_t ncols, const float* norm, cudaStream_t st);
+// tcgen05 screening GEMM, epilogue -> per (row, 128-atom group) the first TOPK entries (|c~_n|, n) within
+// window * resid[row] of the group's maximum, in index order; unused slots (-1, -1); overflow flagged
+cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* status,
+                                const float* resid, float window, float2* part, cudaStream_t st);
 
 // ---- K2 ----
 // a3 over a materialised FP32 C: n*_b = lowest n maximising |C[b,n]| * inv_norm[n]; c* = C[b, n*]
 cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, const float* inv_norm,
                           const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st);
 // ---- setup / init ----
-// K0: atoms -> FP32 copy At (Np x Mp), optional bf16 plane / tf32 hi-lo planes, 1/||a_n||
+// K0: atoms -> FP32 copy At (Np x Mp), ||a_n||, 1/||a_n||, and the screen planes of the NORMALISED
+// atoms a_n / ||a_n|| (optional bf16 plane / tf32 hi-lo planes)
 cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
-                                 float* At, void* At_bf16, float* At_hi, float* At_lo, float* inv_norm,
-                                 int* bad_zero, int* bad_nonfinite, cudaStream_t st);
+                                 float* At, void* At_bf16, float* At_hi, float* At_lo, float* norm,
+                                 float* inv_norm, int* bad_zero, int* bad_nonfinite, cudaStream_t st);
 // row-major fp32 matrix -> padded planes (fp32 copy, optional bf16, optional hi/lo)
 cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp, float* R32,
                                void* Rb, float* R_hi, float* R_lo, cudaStream_t st);
@@ -74,7 +76,7 @@ struct UpdateLaunch {
   float eps;
   int64_t B, N, M, Mp;
   const float2* part;      // screen partials (tensor-core modes) or nullptr (then nstar/cstar are used)
-  int tiles_n;
+  int groups;              // screen partial groups per row (Np / SCREEN_GROUP)
   float window;
   const int32_t* nstar;
   const float* cstar;
