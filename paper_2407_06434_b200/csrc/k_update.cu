@@ -30,6 +30,7 @@
 // return at once (capture-and-continue).
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "omp_internal.cuh"
 
@@ -71,7 +72,8 @@ struct UpdateArgs {
   int32_t* n_iter;
   int32_t* status;
   int f_stage;          // 1: stage F_k in shared memory (else read F from global)
-  int region_floats;    // floats of the aliased residual-row / F region
+  int region_floats;    // floats of the aliased residual-row / F / gather-ring region
+  int ring_slots;       // > 0: bulk-async gather through this many atom-row slots (else LDG gather)
 };
 
 struct Cand {
@@ -119,6 +121,31 @@ __device__ __forceinline__ void stg_policy(float4* ptr, float4 v, uint64_t pol) 
 __device__ __forceinline__ void stg_policy(uint2* ptr, uint2 v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
                ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+
+// one contiguous atom row global -> shared through the bulk-copy (TMA) engine, completing on `bar`
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol) : "memory");
+}
+
+constexpr int MAX_RING = 16;
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
 template <int T>
@@ -177,6 +204,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   __shared__ int sel_n;
   __shared__ float sel_c;
   __shared__ __align__(8) uint64_t fbar;
+  __shared__ __align__(8) uint64_t rfull[MAX_RING], rempty[MAX_RING];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* Fg = a.F + b * a.ldf;
   const uint32_t fbytes = (uint32_t)((((int64_t)k * (k + 1) / 2) + 3) / 4 * 16);
@@ -188,6 +216,29 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&fbar)) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+  }
+
+  // ---- issue every load that does not depend on the selection (one round trip instead of a chain):
+  // support and u of the current factor and (REFINE) the residual row -> shared memory by cp.async;
+  // F_k -> L1 (both passes of the append read it); y -> L2 (the residual phase reads it)
+  for (int j = tid; j < k; j += T) {
+    cp_async4(&ss[j], a.support + b * a.lds + j);
+    cp_async4(&u[j], a.U + b * a.ldu + j);
+  }
+  if constexpr (REFINE) {
+    const float4* r4g = reinterpret_cast<const float4*>(a.R32 + b * a.Mp);
+    for (int q = tid; q < q4; q += T) cp_async16(&rsm[q], r4g + q);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (!staged) {
+    const char* fp = reinterpret_cast<const char*>(Fg);
+    for (uint32_t o = (uint32_t)tid * 128u; o < fbytes; o += (uint32_t)T * 128u)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
+  }
+  {
+    const char* yp = reinterpret_cast<const char*>(a.Y + b * a.ldy);
+    for (int64_t o = (int64_t)tid * 128; o < a.M * 4; o += (int64_t)T * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
   }
 
   // ---- a3: selection ------------------------------------------------------------------------------
@@ -205,7 +256,8 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
 #pragma unroll
     for (int i = 1; i < T / 32; ++i) vmax = fmaxf(vmax, red[i]);
     // every finite, nonzero residual leaves >= 1 entry per group (the group maximum itself); no entry
-    // at all means the screened correlations were NaN
+    // at all means the screened correlations were NaN.  (No CTA may exit with a cp.async in flight.)
+    if (!(vmax >= 0.f) || !isfinite(rn) || rn == 0.f) asm volatile("cp.async.wait_all;" ::: "memory");
     if (!(vmax >= 0.f) || !isfinite(rn)) {
       if (tid == 0) a.status[b] = OMP_SIG_NAN;
       return;
@@ -240,8 +292,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
         }
       }
     }
-    const float4* r4g = reinterpret_cast<const float4*>(a.R32 + b * a.Mp);
-    for (int q = tid; q < q4; q += T) rsm[q] = r4g[q];
+    asm volatile("cp.async.wait_all;" ::: "memory");   // residual row (and ss, u) landed
     full = __syncthreads_or(full);
     Cand best{-1.f, 0x7fffffff, 0.f};
     bool nan_c = false;
@@ -281,6 +332,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
                  ::"r"(smem_addr(Fs)), "l"(Fg), "r"(fbytes), "r"(smem_addr(&fbar))
                  : "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");     // ss, u (SIMT path: first wait)
   __syncthreads();
   const int n = sel_n;
   const float cst = sel_c;
@@ -302,12 +354,10 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   const float* grow = a.G + (int64_t)n * a.ldg;
   bool dup = false;
   for (int j = tid; j < k; j += T) {
-    const int s = a.support[b * a.lds + j];
-    ss[j] = s;
+    const int s = ss[j];
     ro[j] = (uint32_t)s * (uint32_t)q4;
     dup |= (s == n);
     w[j] = grow[s];                     // [A^T A]_{n*, s_j}
-    u[j] = a.U[b * a.ldu + j];
   }
   if (__syncthreads_or(dup)) {          // re-selection (reading R6); let the F copy land first
     wait_f();
@@ -372,7 +422,48 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* A4 = reinterpret_cast<const float4*>(a.At) + tid;
-  if (T * CH == q4) {
+  if (a.ring_slots > 0) {
+    // Bulk-async gather: thread 0 streams whole atom rows (Mp floats, contiguous) into a ring of
+    // shared-memory slots with cp.async.bulk (evict_last L2 policy); every thread folds x_j times its
+    // float4 chunks of row j out of shared memory.  In-flight bytes are bounded by the ring, not by
+    // the register file.  The ring aliases the F / residual-row region, free at this point.
+    const int NS = a.ring_slots;
+    const uint32_t rowb = (uint32_t)(a.Mp * 4);
+    float4* ring = reinterpret_cast<float4*>(dsm);
+    if (tid == 0) {
+      for (int s = 0; s < NS; ++s) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&rfull[s])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&rempty[s])), "r"(T / 32) : "memory");
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of F -> async writes
+      for (int j = 0; j < NS && j < kk; ++j) bulk_row(ring + (size_t)j * q4, A4 - tid + ro[j], rowb, &rfull[j], keep);
+    }
+    __syncthreads();
+    for (int j = 0; j < kk; ++j) {
+      const int s = j % NS;
+      const uint32_t par = (uint32_t)((j / NS) & 1);
+      mbar_wait_parity(&rfull[s], par);
+      const float xj = xs[j];
+      const float4* row = ring + (size_t)s * q4 + tid;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (T * CH == q4 || tid + c * T < q4) {
+          const float4 v = row[c * T];
+          acc[c].x = fmaf(xj, v.x, acc[c].x);
+          acc[c].y = fmaf(xj, v.y, acc[c].y);
+          acc[c].z = fmaf(xj, v.z, acc[c].z);
+          acc[c].w = fmaf(xj, v.w, acc[c].w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&rempty[s])) : "memory");
+      if (tid == 0 && j + NS < kk) {
+        mbar_wait_parity(&rempty[s], par);          // every warp has read slot s
+        bulk_row(ring + (size_t)s * q4, A4 - tid + ro[j + NS], rowb, &rfull[s], keep);
+      }
+    }
+  } else if (T * CH == q4) {
     int j = 0;
     for (; j + 2 <= kk; j += 2) {
       const float4* r0 = A4 + ro[j];
@@ -520,8 +611,28 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) / 4 * 4;
   const bool refine = L.part != nullptr;
   const int64_t rowf = refine ? L.Mp : 0;
-  a.f_stage = (fk * 4 <= (int64_t)64 * 1024 && L.ldf % 4 == 0) ? 1 : 0;
-  a.region_floats = (int)((a.f_stage && fk > rowf) ? fk : rowf);
+  // F_k staging in shared memory (OMP_B200_F_STAGE=1) costs occupancy; by default F_k is prefetched
+  // into L1 at kernel start instead
+  static int fstage_env = -1;
+  if (fstage_env < 0) {
+    const char* env = getenv("OMP_B200_F_STAGE");
+    fstage_env = (env && env[0] == '1') ? 1 : 0;
+  }
+  a.f_stage = (fstage_env && fk * 4 <= (int64_t)64 * 1024 && L.ldf % 4 == 0) ? 1 : 0;
+  int64_t region = (a.f_stage && fk > rowf) ? fk : rowf;
+  // gather ring: OMP_B200_RING_KB (default 48) of atom-row slots, 2..MAX_RING slots; 0 -> LDG gather
+  static int ring_kb = -1;
+  if (ring_kb < 0) {
+    const char* env = getenv("OMP_B200_RING_KB");
+    ring_kb = env ? atoi(env) : 0;   // measured slower than the LDG gather at c4
+  }
+  const int64_t rowf_all = L.Mp;
+  int slots = (int)(((int64_t)ring_kb * 1024 / 4) / rowf_all);
+  if (slots > MAX_RING) slots = MAX_RING;
+  if (slots < 2 || (int64_t)L.Mp * 4 % 16 != 0) slots = 0;
+  a.ring_slots = slots;
+  if (slots * rowf_all > region) region = slots * rowf_all;
+  a.region_floats = (int)region;
   const int64_t Sp = (L.k + 4) & ~3;
   const size_t smem = (size_t)a.region_floats * 4 + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
   return refine ? launch_r<true>(a, L.B, smem, L.l2_persist_bytes, st)
