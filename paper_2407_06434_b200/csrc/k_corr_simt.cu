@@ -13,7 +13,13 @@ constexpr int SB = 128, SN = 128, SK = 16, SPAD = 4;
 
 __global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rm, int64_t ldr, int64_t B,
                                                     const float* __restrict__ Am, int64_t lda, int64_t NA,
-                                                    int64_t K, float* __restrict__ C, int64_t ldc, int64_t ncols) {
+                                                    int64_t K, float* __restrict__ C, int64_t ldc, int64_t ncols,
+                                                    const int32_t* __restrict__ live_rows) {
+  if (live_rows) {                      // live-set compaction: only the first *live_rows rows are live
+    const int64_t lr = *live_rows;
+    if (lr < B) B = lr;
+    if ((int64_t)blockIdx.y * SB >= B) return;
+  }
   __shared__ float As[SK][SB + SPAD];   // R tile, transposed: As[k][row]
   __shared__ float Bs[SK][SN + SPAD];   // At tile, transposed: Bs[k][atom]
   const int tid = threadIdx.x;
@@ -75,14 +81,14 @@ __global__ void __launch_bounds__(256) k1_corr_simt(const float* __restrict__ Rm
 }
 
 cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
-                             int64_t ncols, cudaStream_t st) {
+                             int64_t ncols, const int32_t* live_rows, cudaStream_t st) {
   if (R.rows == 0) return cudaSuccess;
   if (K % SK != 0 || R.ld % 4 != 0 || At.ld % 4 != 0) return cudaErrorInvalidValue;
   if (ncols > At.rows) ncols = At.rows;
   dim3 grid((unsigned)((ncols + SN - 1) / SN), (unsigned)((R.rows + SB - 1) / SB));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k1_corr_simt<<<grid, 256, 0, st>>>((const float*)R.plane[0], R.ld, R.rows, (const float*)At.plane[0], At.ld,
-                                     At.rows, K, C, ldc, ncols);
+                                     At.rows, K, C, ldc, ncols, live_rows);
   return cudaGetLastError();
 }
 

@@ -203,8 +203,8 @@ struct EpiArgs {
   int64_t ncols;            // columns < ncols are stored
   const float* norm;        // MODE_STORE: ||a_n|| (the screen runs on normalised atoms)
   float2* part;             // MODE_TOPK: rows x (2 tiles_n) x TOPK {value, index bits}
-  const int32_t* status;    // MODE_TOPK: finished rows are skipped (may be null)
-  const float* resid;       // MODE_TOPK: ||r_b|| of the residual being screened
+  const int32_t* live_rows; // rows < *live_rows are live (live-set compaction); null: all rows
+  const float* rslot;       // MODE_TOPK: ||r|| of the residual in each row
   float window;             // MODE_TOPK: screening window / ||r||
 };
 
@@ -216,6 +216,13 @@ struct Maps {
 template <int KIND, int CG, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m, int tiles_n, EpiArgs ep) {
+  // live-set compaction: the live rows are the first *live_rows rows of the buffer; the grid was sized
+  // for the buffer's capacity and the clusters without a live tile have nothing to do
+  if (ep.live_rows) {
+    const int lr = *ep.live_rows;
+    if (lr < rows) rows = lr;
+    tiles_m = (rows + BM * CG - 1) / (BM * CG);
+  }
   using C_ = Cfg<KIND, CG>;
   using K_ = Kind<KIND>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -359,8 +366,7 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
         // reaching max - W and emit their in-window entries in index order (predicated stores; at
         // most TOPK, an overflow is flagged in the last slot with the half-tile maximum).
         float W = 0.f;
-        if (live && ep.status) live = ep.status[row] == SIG_RUNNING;
-        if (live) W = ep.window * ep.resid[row];
+        if (live) W = ep.window * ep.rslot[row];
         float cm[HB / 32];
         float tmax = 0.f;
 #pragma unroll
@@ -515,13 +521,13 @@ static cudaError_t dispatch(int kind, const Operand& R, const Operand& At, int64
 
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, const float* norm, cudaStream_t st) {
-  tc::EpiArgs ep{C, ldc, ncols, norm, nullptr, nullptr, nullptr, 0.f};
+  tc::EpiArgs ep{C, ldc, ncols, norm, nullptr, nullptr, nullptr, 0.f};   // all rows, no compaction
   return tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
 }
 
-cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* status,
-                                const float* resid, float window, float2* part, cudaStream_t st) {
-  tc::EpiArgs ep{nullptr, 0, At.rows, nullptr, part, status, resid, window};
+cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* live_rows,
+                                const float* rslot, float window, float2* part, cudaStream_t st) {
+  tc::EpiArgs ep{nullptr, 0, At.rows, nullptr, part, live_rows, rslot, window};
   return tc::dispatch<tc::MODE_TOPK>(kind, R, At, K, ep, st);
 }
 

@@ -19,11 +19,12 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k2_select(const float* __restrict__ C, int64_t ldc, int64_t N,
                                                      const float* __restrict__ inv_norm,
                                                      const int32_t* __restrict__ status,
+                                                     const int32_t* __restrict__ slot,
                                                      int32_t* __restrict__ nstar, float* __restrict__ cstar,
                                                      bool vec) {
   const int64_t b = blockIdx.x;
   if (status[b] != SIG_RUNNING) return;
-  const float* c = C + b * ldc;
+  const float* c = C + (int64_t)slot[b] * ldc;   // the signal's row in the live set
   Best best{-1.f, 0x7fffffff};
   bool nan_seen = false;
   if (vec) {
@@ -77,14 +78,15 @@ __global__ void __launch_bounds__(THREADS) k2_select(const float* __restrict__ C
 }
 
 cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, const float* inv_norm,
-                          const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st) {
+                          const int32_t* status, const int32_t* slot, int32_t* nstar, float* cstar,
+                          cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(inv_norm) & 15) == 0);
   if (N >= 2048)
-    k2_select<256><<<(unsigned)B, 256, 0, st>>>(C, ldc, N, inv_norm, status, nstar, cstar, vec);
+    k2_select<256><<<(unsigned)B, 256, 0, st>>>(C, ldc, N, inv_norm, status, slot, nstar, cstar, vec);
   else
-    k2_select<128><<<(unsigned)B, 128, 0, st>>>(C, ldc, N, inv_norm, status, nstar, cstar, vec);
+    k2_select<128><<<(unsigned)B, 128, 0, st>>>(C, ldc, N, inv_norm, status, slot, nstar, cstar, vec);
   return cudaGetLastError();
 }
 

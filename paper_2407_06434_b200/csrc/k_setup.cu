@@ -104,20 +104,23 @@ cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M
 }
 
 // a1: x_0 = 0, r_0 = y; eps is tested on r_0 (reading R2);
-// support = -1, n_iter = 0.  One CTA per signal.
+// support = -1, n_iter = 0.  One CTA per signal.  A signal that is still running takes the next
+// slot of the live set (atomic counter live0): its planes go to that row, so the first correlation
+// only covers running signals (live-set compaction).
 __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M, int64_t Mp, int32_t S, float eps,
                              float* __restrict__ R32, __nv_bfloat16* __restrict__ Rb, float* __restrict__ Rhi,
                              float* __restrict__ Rlo, float* __restrict__ X, int64_t ldx,
                              int32_t* __restrict__ support, int64_t lds, float* __restrict__ resid,
-                             int32_t* __restrict__ n_iter, int32_t* __restrict__ status) {
+                             int32_t* __restrict__ n_iter, int32_t* __restrict__ status, int32_t* __restrict__ slot,
+                             int32_t* __restrict__ live0, float* __restrict__ rslot) {
   __shared__ double red[32];
+  __shared__ int s_slot;
   const int64_t b = blockIdx.x;
   const float* y = Y + b * ldy;
   float part = 0.f;
-  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
-    const float v = m < M ? y[m] : 0.f;
+  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+    const float v = y[m];
     part = fmaf(v, v, part);
-    put_planes(b * Mp + m, v, R32, Rb, Rhi, Rlo);
   }
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     X[b * ldx + j] = 0.f;
@@ -127,23 +130,36 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
   if (threadIdx.x == 0) {
     const float rn = (float)sqrt(ss);
     n_iter[b] = 0;
+    int st;
     if (!isfinite(ss)) {
-      status[b] = OMP_SIG_NAN;
+      st = OMP_SIG_NAN;
       resid[b] = nanf("");
     } else {
       resid[b] = rn;
-      status[b] = (eps >= 0.f && rn <= eps) ? OMP_SIG_EPS : SIG_RUNNING;
+      st = (eps >= 0.f && rn <= eps) ? OMP_SIG_EPS : SIG_RUNNING;
     }
+    status[b] = st;
+    s_slot = -1;
+    if (st == SIG_RUNNING) {
+      s_slot = atomicAdd(live0, 1);
+      rslot[s_slot] = rn;
+    }
+    slot[b] = s_slot;
   }
+  __syncthreads();
+  const int sl = s_slot;
+  if (sl < 0) return;
+  for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x)
+    put_planes((int64_t)sl * Mp + m, m < M ? y[m] : 0.f, R32, Rb, Rhi, Rlo);
 }
 
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
-                              cudaStream_t st) {
+                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   k_batch_init<<<(unsigned)B, 128, 0, st>>>(Y, ldy, M, Mp, S, eps, R32, (__nv_bfloat16*)Rb, R_hi, R_lo, X, ldx,
-                                            support, lds, resid, n_iter, status);
+                                            support, lds, resid, n_iter, status, slot, live0, rslot);
   return cudaGetLastError();
 }
 

@@ -64,10 +64,14 @@ struct UpdateArgs {
   int64_t ldx;
   int32_t* support;
   int64_t lds;
-  float* R32;
+  const float* R32in;   // current residual rows (row = slot)
+  float* R32;           // next residual planes (row = new slot)
   __nv_bfloat16* Rb;
   float* Rhi;
   float* Rlo;
+  float* rslot_out;
+  int32_t* slot;
+  int32_t* live_next;
   float* resid;
   int32_t* n_iter;
   int32_t* status;
@@ -185,6 +189,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   const int k = a.k;
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
+  const int cur_slot = a.slot[b];       // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update):
   //   [region X: the fp32 residual row (refine) then the packed F_k prefix (append), aliased]
   //   [w, z, u, xs: Sp floats each] [ss: Sp ints] [cand: RF_CAP ints (refine)]
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
     cp_async4(&u[j], a.U + b * a.ldu + j);
   }
   if constexpr (REFINE) {
-    const float4* r4g = reinterpret_cast<const float4*>(a.R32 + b * a.Mp);
+    const float4* r4g = reinterpret_cast<const float4*>(a.R32in + (int64_t)cur_slot * a.Mp);
     for (int q = tid; q < q4; q += T) cp_async16(&rsm[q], r4g + q);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
     const float rn = a.resid[b];
-    const float2* P = a.part + b * (int64_t)a.groups * TOPK;
+    const float2* P = a.part + (int64_t)cur_slot * a.groups * TOPK;
     const int E = a.groups * TOPK;
     float vmax = -1.f;
     for (int e = tid; e < E; e += T) vmax = fmaxf(vmax, P[e].x);
@@ -527,21 +532,8 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
         yv.z = m + 2 < a.M ? y[m + 2] : 0.f;
         yv.w = m + 3 < a.M ? y[m + 3] : 0.f;
       }
-      const float4 r = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
-      part = fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, fmaf(r.w, r.w, part))));
-      if (a.R32) stg_policy(reinterpret_cast<float4*>(a.R32 + b * a.Mp) + q, r, stream);
-      if (a.Rb) {
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&p0);
-        pk.y = *reinterpret_cast<uint32_t*>(&p1);
-        stg_policy(reinterpret_cast<uint2*>(a.Rb + b * a.Mp) + q, pk, stream);
-      }
-      if (a.Rhi) {
-        const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
-        reinterpret_cast<float4*>(a.Rhi + b * a.Mp)[q] = h;
-        reinterpret_cast<float4*>(a.Rlo + b * a.Mp)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
-      }
+      acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);   // r
+      part = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, fmaf(acc[c].w, acc[c].w, part))));
     }
   }
   const float rr = block_sum<T>(part, red);
@@ -549,8 +541,39 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
     const float rn = sqrtf(rr);
     a.resid[b] = rn;
     a.n_iter[b] = kk;
+    int ns = -1;
     if (a.eps >= 0.f && rn <= a.eps) a.status[b] = OMP_SIG_EPS;
     else if (kk == a.S) a.status[b] = OMP_SIG_MAXITER;
+    else {
+      ns = atomicAdd(a.live_next, 1);                                  // next live-set slot
+      a.rslot_out[ns] = rn;
+    }
+    a.slot[b] = ns;
+    sel_n = ns;
+  }
+  __syncthreads();
+  const int ns = sel_n;
+  if (ns < 0) return;                   // finished: no planes for the next screen
+  const int64_t ro_out = (int64_t)ns * a.Mp;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int q = tid + c * T;
+    if (q < q4) {
+      const float4 r = acc[c];
+      if (a.R32) stg_policy(reinterpret_cast<float4*>(a.R32 + ro_out) + q, r, stream);
+      if (a.Rb) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&p0);
+        pk.y = *reinterpret_cast<uint32_t*>(&p1);
+        stg_policy(reinterpret_cast<uint2*>(a.Rb + ro_out) + q, pk, stream);
+      }
+      if (a.Rhi) {
+        const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
+        reinterpret_cast<float4*>(a.Rhi + ro_out)[q] = h;
+        reinterpret_cast<float4*>(a.Rlo + ro_out)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
+      }
+    }
   }
 }
 
@@ -605,8 +628,9 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.part = L.part; a.groups = L.groups; a.window = L.window; a.nstar = L.nstar; a.cstar = L.cstar;
   a.At = L.At; a.inv_norm = L.inv_norm; a.G = L.G; a.ldg = L.ldg;
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
-  a.support = L.support; a.lds = L.lds; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb; a.Rhi = L.Rhi;
-  a.Rlo = L.Rlo; a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status;
+  a.support = L.support; a.lds = L.lds; a.R32in = L.R32in; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb;
+  a.Rhi = L.Rhi; a.Rlo = L.Rlo; a.rslot_out = L.rslot_out; a.slot = L.slot; a.live_next = L.live_next;
+  a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status;
   // one region holds the residual row (refine) and then F_k (append); F is staged when it fits
   const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) / 4 * 4;
   const bool refine = L.part != nullptr;

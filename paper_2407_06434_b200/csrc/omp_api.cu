@@ -42,8 +42,13 @@ struct ompHandle_st {
   // batch workspace
   int64_t capB = 0;
   int32_t capS = 0;
+  // residual planes, double-buffered (iteration k reads buffer k&1 and writes buffer (k+1)&1) and
+  // compacted: the live signals occupy rows [0, live[k]) in slot order (slot[b])
   float *R32 = nullptr, *R_hi = nullptr, *R_lo = nullptr, *C = nullptr, *F = nullptr, *U = nullptr;
   uint16_t* Rb = nullptr;  // bf16 plane of the residuals
+  float* rslot = nullptr;  // ||r|| per row, double-buffered
+  int32_t* slot = nullptr; // signal -> row of the current buffer (-1: finished)
+  int32_t* live = nullptr; // live[k] = rows of the buffer screened at iteration k (device counters)
   int32_t* nstar = nullptr;
   float* cstar = nullptr;
   float2* part = nullptr;   // screening epilogue: (B) x (Np / 128) x TOPK candidates
@@ -122,10 +127,15 @@ static Operand atoms_operand(const ompHandle_t h) {
   if (tc_kind(h) == KIND_BF16) return Operand{{h->Ab, nullptr}, h->Np, h->Mp};
   return Operand{{h->At_hi, h->At_lo}, h->Np, h->Mp};
 }
-static Operand resid_operand(const ompHandle_t h, int64_t B) {
-  if (!tc_mode(h)) return Operand{{h->R32, nullptr}, B, h->Mp};
-  if (tc_kind(h) == KIND_BF16) return Operand{{h->Rb, nullptr}, B, h->Mp};
-  return Operand{{h->R_hi, h->R_lo}, B, h->Mp};
+// buffer `buf` of the residual planes (capacity capB rows each)
+static float* r32_buf(const ompHandle_t h, int buf) { return h->R32 + (size_t)buf * h->capB * h->Mp; }
+static uint16_t* rb_buf(const ompHandle_t h, int buf) { return h->Rb ? h->Rb + (size_t)buf * h->capB * h->Mp : nullptr; }
+static float* rhi_buf(const ompHandle_t h, int buf) { return h->R_hi ? h->R_hi + (size_t)buf * h->capB * h->Mp : nullptr; }
+static float* rlo_buf(const ompHandle_t h, int buf) { return h->R_lo ? h->R_lo + (size_t)buf * h->capB * h->Mp : nullptr; }
+static Operand resid_operand(const ompHandle_t h, int64_t B, int buf) {
+  if (!tc_mode(h)) return Operand{{r32_buf(h, buf), nullptr}, B, h->Mp};
+  if (tc_kind(h) == KIND_BF16) return Operand{{rb_buf(h, buf), nullptr}, B, h->Mp};
+  return Operand{{rhi_buf(h, buf), rlo_buf(h, buf)}, B, h->Mp};
 }
 
 // rigorous screening bound c0 (|c~ - c| <= c0 ||a|| ||r||) + the FP32 re-evaluation bound,
@@ -167,16 +177,19 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   const int32_t nS = S > h->capS ? S : h->capS;
   const int64_t ldf = round_up((int64_t)nS * (nS + 1) / 2, 4);   // 16-byte aligned rows for the bulk copy
   const bool tc = tc_mode(h), bf = tc && tc_kind(h) == KIND_BF16, x3 = tc && !bf;
-  bool ok = dalloc(h->R32, (size_t)nB * h->Mp) && dalloc(h->F, (size_t)nB * ldf) &&
-            dalloc(h->U, (size_t)nB * nS) && dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB);
-  if (ok && bf) ok = dalloc(h->Rb, (size_t)nB * h->Mp);
-  if (ok && x3) ok = dalloc(h->R_hi, (size_t)nB * h->Mp) && dalloc(h->R_lo, (size_t)nB * h->Mp);
+  const size_t planes = 2 * (size_t)nB * h->Mp;                  // two buffers
+  bool ok = dalloc(h->R32, planes) && dalloc(h->F, (size_t)nB * ldf) && dalloc(h->U, (size_t)nB * nS) &&
+            dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB) && dalloc(h->rslot, 2 * (size_t)nB) &&
+            dalloc(h->slot, (size_t)nB) && dalloc(h->live, (size_t)nS + 2);
+  if (ok && bf) ok = dalloc(h->Rb, planes);
+  if (ok && x3) ok = dalloc(h->R_hi, planes) && dalloc(h->R_lo, planes);
   if (ok && tc) ok = dalloc(h->part, (size_t)nB * (h->Np / SCREEN_GROUP) * TOPK);
   if (ok && !tc) ok = dalloc(h->C, (size_t)nB * h->Np);
   h->capC = (ok && !tc) ? nB : 0;
   if (!ok) {
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->C); dfree(h->F); dfree(h->U);
-    dfree(h->nstar); dfree(h->cstar); dfree(h->part); dfree(h->Rb);
+    dfree(h->nstar); dfree(h->cstar); dfree(h->part); dfree(h->Rb); dfree(h->rslot); dfree(h->slot);
+    dfree(h->live);
     h->capB = 0;
     h->capS = 0;
     cudaGetLastError();
@@ -196,30 +209,34 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
   if (s != OMP_OK) return s;
   if (!(eps >= 0.f)) eps = -1.f;   // NaN or negative: no tolerance
   Launcher L{h, st};
-  cudaError_t e;
+  cudaError_t e = cudaMemsetAsync(h->live, 0, sizeof(int32_t) * ((size_t)S + 2), st);
+  if (e != cudaSuccess) return cuda_fail(h, e);
   L.begin(0);
-  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, h->R32, h->Rb, h->R_hi, h->R_lo, X, ldx, support, lds,
-                        resid, n_iter, status, st);
+  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, r32_buf(h, 0), rb_buf(h, 0), rhi_buf(h, 0), rlo_buf(h, 0),
+                        X, ldx, support, lds, resid, n_iter, status, h->slot, h->live, h->rslot, st);
   L.end(0);
   if (e != cudaSuccess) return cuda_fail(h, e);
-  const Operand R = resid_operand(h, B), At = atoms_operand(h);
+  const Operand At = atoms_operand(h);
   for (int32_t k = 0; k < S; ++k) {
+    const int cur = k & 1, nxt = cur ^ 1;
+    const Operand R = resid_operand(h, B, cur);
     if (tc_mode(h)) {
-      // a2: tensor-core screen C~ = A^T R_k; the epilogue keeps per 256-atom tile the top-4 entries
-      // within the screening window of the tile maximum
+      // a2: tensor-core screen C~ = A^T R_k over the live rows; the epilogue keeps the in-window
+      // entries of every 128-atom group
       L.begin(1);
-      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, status, resid, h->window, h->part, st);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->live + k, h->rslot + (size_t)cur * h->capB, h->window,
+                              h->part, st);
       L.end(1);
       if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
       if (e != cudaSuccess) return cuda_fail(h, e);
     } else {
-      // a2: FP32 SIMT GEMM C = A^T R_k; a3: n* = argmax |c_n| / ||a_n|| over the materialised C
+      // a2: FP32 SIMT GEMM C = A^T R_k over the live rows; a3: n* = argmax |c_n| / ||a_n||
       L.begin(1);
-      e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, st);
+      e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, h->live + k, st);
       L.end(1);
       if (e != cudaSuccess) return cuda_fail(h, e);
       L.begin(2);
-      e = launch_select(h->C, h->Np, B, h->N, h->inv_norm, status, h->nstar, h->cstar, st);
+      e = launch_select(h->C, h->Np, B, h->N, h->inv_norm, status, h->slot, h->nstar, h->cstar, st);
       L.end(2);
       if (e != cudaSuccess) return cuda_fail(h, e);
     }
@@ -234,7 +251,10 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
     U.Y = Y; U.ldy = ldy; U.F = h->F; U.ldf = h->ldf; U.U = h->U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
     U.support = support; U.lds = lds;
-    U.R32 = h->R32; U.Rb = h->Rb; U.Rhi = h->R_hi; U.Rlo = h->R_lo;
+    U.R32in = r32_buf(h, cur);
+    U.R32 = r32_buf(h, nxt); U.Rb = rb_buf(h, nxt); U.Rhi = rhi_buf(h, nxt); U.Rlo = rlo_buf(h, nxt);
+    U.rslot_out = h->rslot + (size_t)nxt * h->capB;
+    U.slot = h->slot; U.live_next = h->live + k + 1;
     U.resid = resid; U.n_iter = n_iter; U.status = status;
     U.l2_persist_bytes = h->l2_persist;
     L.begin(3);
@@ -290,6 +310,7 @@ ompStatus_t ompDestroy(ompHandle_t h) {
     dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->norm); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
+    dfree(h->rslot); dfree(h->slot); dfree(h->live);
     dfree(h->nstar); dfree(h->cstar); dfree(h->part);
     dfree(h->hY); dfree(h->hX); dfree(h->hres); dfree(h->hsup); dfree(h->hnit); dfree(h->hst);
     for (auto& r : h->prof_pending) {
@@ -375,7 +396,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   // Gram matrix G = A^T A in FP32 with round-to-nearest accumulation (the
   // truncating tensor-core accumulator would bias ||a||^2 - ||z||^2)
   const Operand A32{{h->At, nullptr}, h->Np, h->Mp};
-  e = launch_corr_simt(A32, A32, h->Mp, h->G, h->Np, h->Np, st);
+  e = launch_corr_simt(A32, A32, h->Mp, h->G, h->Np, h->Np, nullptr, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     ompStatus_t s = cuda_fail(nullptr, e);
@@ -463,11 +484,12 @@ ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, 
     }
     h->capC = B;
   }
-  cudaError_t e = launch_make_planes(R, B, ldr, h->M, h->Mp, h->R32, h->Rb, h->R_hi, h->R_lo, st);
-  const Operand Rop = resid_operand(h, B), At = atoms_operand(h);
+  cudaError_t e = launch_make_planes(R, B, ldr, h->M, h->Mp, r32_buf(h, 0), rb_buf(h, 0), rhi_buf(h, 0),
+                                     rlo_buf(h, 0), st);
+  const Operand Rop = resid_operand(h, B, 0), At = atoms_operand(h);
   if (e == cudaSuccess)
     e = tc_mode(h) ? launch_corr_tc(tc_kind(h), Rop, At, h->Mp, h->C, h->Np, h->Np, h->norm, st)
-                   : launch_corr_simt(Rop, At, h->Mp, h->C, h->Np, h->Np, st);
+                   : launch_corr_simt(Rop, At, h->Mp, h->C, h->Np, h->Np, nullptr, st);
   if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(C, ldc * sizeof(float), h->C, h->Np * sizeof(float), h->N * sizeof(float), B,

@@ -40,21 +40,24 @@ struct Operand {
 };
 
 // ---- K1: correlation C[b, n] = sum_k R[b, k] * At[n, k] ----
-// FP32 SIMT GEMM (round-to-nearest, sequential K): C written for rows < R.rows, n < ncols
+// Row counts: R.rows is the buffer's capacity; `live_rows` (device, may be null) is the number of
+// live rows at the top of the buffer when the kernel runs (live-set compaction).
+// FP32 SIMT GEMM (round-to-nearest, sequential K): C written for rows < live rows, n < ncols
 cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
-                             int64_t ncols, cudaStream_t st);
+                             int64_t ncols, const int32_t* live_rows, cudaStream_t st);
 // tcgen05 screening GEMM on normalised atoms; C~ stored times ||a_n|| (diagnostics / numerics tests)
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, const float* norm, cudaStream_t st);
 // tcgen05 screening GEMM, epilogue -> per (row, 128-atom group) the first TOPK entries (|c~_n|, n) within
-// window * resid[row] of the group's maximum, in index order; unused slots (-1, -1); overflow flagged
-cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* status,
-                                const float* resid, float window, float2* part, cudaStream_t st);
+// window * rslot[row] of the group's maximum, in index order; unused slots (-1, -1); overflow flagged
+cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* live_rows,
+                                const float* rslot, float window, float2* part, cudaStream_t st);
 
 // ---- K2 ----
-// a3 over a materialised FP32 C: n*_b = lowest n maximising |C[b,n]| * inv_norm[n]; c* = C[b, n*]
+// a3 over a materialised FP32 C (row slot[b]): n*_b = lowest n maximising |C[row,n]| * inv_norm[n]; c* = C[row,n*]
 cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, const float* inv_norm,
-                          const int32_t* status, int32_t* nstar, float* cstar, cudaStream_t st);
+                          const int32_t* status, const int32_t* slot, int32_t* nstar, float* cstar,
+                          cudaStream_t st);
 // ---- setup / init ----
 // K0: atoms -> FP32 copy At (Np x Mp), ||a_n||, 1/||a_n||, and the screen planes of the NORMALISED
 // atoms a_n / ||a_n|| (optional bf16 plane / tf32 hi-lo planes)
@@ -64,11 +67,12 @@ cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t l
 // row-major fp32 matrix -> padded planes (fp32 copy, optional bf16, optional hi/lo)
 cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp, float* R32,
                                void* Rb, float* R_hi, float* R_lo, cudaStream_t st);
-// a1: batch init (also writes the residual planes of r_0 = y)
+// a1: batch init; running signals take live-set slots (atomic counter *live0) and their r_0 = y
+// planes go to row slot[b]; rslot[slot] = ||y||
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
-                              cudaStream_t st);
+                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st);
 
 // ---- a3 + a4 + a5 fused per signal (k_update.cu) ----
 struct UpdateLaunch {
@@ -94,10 +98,14 @@ struct UpdateLaunch {
   int64_t ldx;
   int32_t* support;
   int64_t lds;
-  float* R32;
+  const float* R32in;      // residual planes read at row slot[b] (this iteration's buffer)
+  float* R32;              // residual planes written at the signal's new slot (next iteration's buffer)
   void* Rb;
   float* Rhi;
   float* Rlo;
+  float* rslot_out;        // ||r|| per new slot (the next screen's window)
+  int32_t* slot;           // signal -> row of the current buffer; updated to the new slot
+  int32_t* live_next;      // atomic slot counter of the next buffer
   float* resid;
   int32_t* n_iter;
   int32_t* status;
