@@ -168,15 +168,23 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // lanes of one warp: c = sum_m r[m] a_n[m] in a fixed order (lane-strided float4, xor tree)
 __device__ __forceinline__ float warp_dot(const float4* __restrict__ r4, const float4* __restrict__ a4, int q4,
                                           int lane) {
-  float acc = 0.f;
-  for (int q = lane; q < q4; q += 32) {
+  // four float4 loads in flight per lane, four partial sums (fixed order: deterministic)
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int q = lane;
+  for (; q + 96 < q4; q += 128) {
+    const float4 a0 = __ldg(a4 + q), a1 = __ldg(a4 + q + 32), a2 = __ldg(a4 + q + 64), a3 = __ldg(a4 + q + 96);
+    const float4 r0 = r4[q], r1 = r4[q + 32], r2 = r4[q + 64], r3 = r4[q + 96];
+    s0 = fmaf(r0.x, a0.x, fmaf(r0.y, a0.y, fmaf(r0.z, a0.z, fmaf(r0.w, a0.w, s0))));
+    s1 = fmaf(r1.x, a1.x, fmaf(r1.y, a1.y, fmaf(r1.z, a1.z, fmaf(r1.w, a1.w, s1))));
+    s2 = fmaf(r2.x, a2.x, fmaf(r2.y, a2.y, fmaf(r2.z, a2.z, fmaf(r2.w, a2.w, s2))));
+    s3 = fmaf(r3.x, a3.x, fmaf(r3.y, a3.y, fmaf(r3.z, a3.z, fmaf(r3.w, a3.w, s3))));
+  }
+  for (; q < q4; q += 32) {
     const float4 a = __ldg(a4 + q);
     const float4 r = r4[q];
-    acc = fmaf(r.x, a.x, acc);
-    acc = fmaf(r.y, a.y, acc);
-    acc = fmaf(r.z, a.z, acc);
-    acc = fmaf(r.w, a.w, acc);
+    s0 = fmaf(r.x, a.x, fmaf(r.y, a.y, fmaf(r.z, a.z, fmaf(r.w, a.w, s0))));
   }
+  float acc = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
@@ -371,14 +379,27 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   }
   wait_f();
   const float* Fb = staged ? Fs : Fg;
-  // z_j = F[:, j] . w  (column dot, one warp per column)
-  for (int j = warp; j < k; j += T / 32) {
-    const float* col = Fb + (int64_t)j * (j + 1) / 2;
-    float acc = 0.f;
-    for (int i = lane; i <= j; i += 32) acc = fmaf(col[i], w[i], acc);
+  // z_j = F[:, j] . w  (column dots; a warp takes two columns at a time so their loads and
+  // shuffle reductions overlap)
+  constexpr int NW = T / 32;
+  for (int j0 = 2 * warp; j0 < k; j0 += 2 * NW) {
+    const int j1 = j0 + 1;
+    const float* c0 = Fb + (int64_t)j0 * (j0 + 1) / 2;
+    const float* c1 = Fb + (int64_t)j1 * (j1 + 1) / 2;
+    float a0 = 0.f, a1 = 0.f;
+    for (int i = lane; i <= j1; i += 32) {
+      if (i <= j0) a0 = fmaf(c0[i], w[i], a0);
+      if (j1 < k) a1 = fmaf(c1[i], w[i], a1);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) z[j] = acc;
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane == 0) {
+      z[j0] = a0;
+      if (j1 < k) z[j1] = a1;
+    }
   }
   __syncthreads();
   float zz = 0.f;
@@ -395,12 +416,30 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   // v = F_k z and t = F_k u in one pass over F (thread per row; lanes of a warp share column j)
   float* newcol = a.F + b * a.ldf + (int64_t)k * (k + 1) / 2;
   for (int i = tid; i < k; i += T) {
-    float v = 0.f, t = 0.f;
-    for (int j = i & ~31; j < k; ++j) {
-      const float f = (j >= i) ? Fb[(int64_t)j * (j + 1) / 2 + i] : 0.f;
-      v = fmaf(f, z[j], v);
-      t = fmaf(f, u[j], t);
+    // four independent partial sums so four column loads are in flight per thread
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    int j = i & ~31;
+    for (; j + 4 <= k; j += 4) {
+      const float f0 = (j >= i) ? Fb[(int64_t)j * (j + 1) / 2 + i] : 0.f;
+      const float f1 = (j + 1 >= i) ? Fb[(int64_t)(j + 1) * (j + 2) / 2 + i] : 0.f;
+      const float f2 = (j + 2 >= i) ? Fb[(int64_t)(j + 2) * (j + 3) / 2 + i] : 0.f;
+      const float f3 = (j + 3 >= i) ? Fb[(int64_t)(j + 3) * (j + 4) / 2 + i] : 0.f;
+      v0 = fmaf(f0, z[j], v0);
+      t0 = fmaf(f0, u[j], t0);
+      v1 = fmaf(f1, z[j + 1], v1);
+      t1 = fmaf(f1, u[j + 1], t1);
+      v2 = fmaf(f2, z[j + 2], v2);
+      t2 = fmaf(f2, u[j + 2], t2);
+      v3 = fmaf(f3, z[j + 3], v3);
+      t3 = fmaf(f3, u[j + 3], t3);
     }
+    for (; j < k; ++j) {
+      const float f = (j >= i) ? Fb[(int64_t)j * (j + 1) / 2 + i] : 0.f;
+      v0 = fmaf(f, z[j], v0);
+      t0 = fmaf(f, u[j], t0);
+    }
+    const float v = (v0 + v1) + (v2 + v3);
+    const float t = (t0 + t1) + (t2 + t3);
     newcol[i] = -gamma * v;                       // -gamma F_k z
     const float xi = fmaf(-gamma * v, unew, t);   // x_i = (F_k u)_i + f_i u_new
     a.X[b * a.ldx + i] = xi;
@@ -611,6 +650,12 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
 template <bool REFINE>
 static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   const int64_t q4 = a.Mp / 4;   // float4 chunks per row; T * CH == q4 at powers of two
+  static int wide = -1;          // OMP_B200_UPDATE_WIDE=1: 256 threads per signal at M = 1025..2048
+  if (wide < 0) {
+    const char* env = getenv("OMP_B200_UPDATE_WIDE");
+    wide = (env && env[0] == '1') ? 1 : 0;
+  }
+  if (wide && q4 > 256 && q4 <= 512) return launch_t<REFINE, 256, 2>(a, B, smem, persist, st);
   if (q4 <= 32) return launch_t<REFINE, 32, 1>(a, B, smem, persist, st);
   if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, persist, st);
   if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, persist, st);
