@@ -288,8 +288,8 @@ def main():
                 "work_per_launch": per_launch, "launch_ms": t_launch * 1e3}
     if split:
         # the update kernel's atom gather is served by L2: report the effective-bandwidth split and the
-        # L2 roofline (L2 peak from ncu: lts throughput % on the r01 capture)
-        l2_peak = 25600.0
+        # L2 roofline: ncu lts__t_sectors peak = 3 sectors/clk x 184 slices x 32 B x 1.958 GHz
+        l2_peak = 34600.0
         roofline.update({"hbm_bytes": split["hbm_bytes"], "l2_gather_bytes": split["l2_gather_bytes"],
                          "effective": "achieved = (streamed HBM bytes + L2 gather bytes) / launch time",
                          "l2_peak_gbs": l2_peak, "frac_of_l2_peak": achieved / l2_peak})
