@@ -190,8 +190,10 @@ __device__ __forceinline__ float warp_dot(const float4* __restrict__ r4, const f
   return acc;
 }
 
-template <bool REFINE, int T, int CH>
-__global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
+// MINB: resident CTAs per SM the register budget must allow.  The kernel is latency-bound on its L2
+// gather and needs >= 8 CTAs of 128 threads per SM (measured: 2x slower at fewer, flat above).
+template <bool REFINE, int T, int CH, int MINB = 1024 / T>
+__global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int64_t b = blockIdx.x;
   if (a.status[b] != SIG_RUNNING) return;
   const int k = a.k;
@@ -616,9 +618,9 @@ __global__ void __launch_bounds__(T) k_update(const UpdateArgs a) {
   }
 }
 
-template <bool REFINE, int T, int CH>
+template <bool REFINE, int T, int CH, int MINB = 1024 / T>
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
-  auto kern = k_update<REFINE, T, CH>;
+  auto kern = k_update<REFINE, T, CH, MINB>;
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   static bool opted = false;
   if (!opted) {
@@ -660,7 +662,16 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, persist, st);
   if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, persist, st);
   if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, persist, st);
-  if (q4 <= 512) return launch_t<REFINE, 128, 4>(a, B, smem, persist, st);
+  if (q4 <= 512) {
+    static int minb = -1;          // OMP_B200_UPDATE_MINB: register budget for 10 or 12 CTAs per SM
+    if (minb < 0) {
+      const char* env = getenv("OMP_B200_UPDATE_MINB");
+      minb = env ? atoi(env) : 0;
+    }
+    if (minb == 10) return launch_t<REFINE, 128, 4, 10>(a, B, smem, persist, st);
+    if (minb == 12) return launch_t<REFINE, 128, 4, 12>(a, B, smem, persist, st);
+    return launch_t<REFINE, 128, 4>(a, B, smem, persist, st);
+  }
   if (q4 <= 1024) return launch_t<REFINE, 256, 4>(a, B, smem, persist, st);
   if (q4 <= 2048) return launch_t<REFINE, 256, 8>(a, B, smem, persist, st);
   return cudaErrorNotSupported;   // M > 8192

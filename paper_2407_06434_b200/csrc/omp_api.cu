@@ -29,6 +29,19 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 
+// everything a captured batch bakes in
+struct GraphKey {
+  int64_t B, ldy, ldx, lds;
+  int32_t S;
+  float eps;
+  const void *Y, *X, *support, *resid, *n_iter, *status;
+  bool operator==(const GraphKey& o) const {
+    return B == o.B && ldy == o.ldy && ldx == o.ldx && lds == o.lds && S == o.S &&
+           (eps == o.eps || (eps != eps && o.eps != o.eps)) && Y == o.Y && X == o.X && support == o.support &&
+           resid == o.resid && n_iter == o.n_iter && status == o.status;
+  }
+};
+
 struct ompHandle_st {
   int device = 0;
   int64_t M = 0, N = 0, Mp = 0, Np = 0;
@@ -67,6 +80,19 @@ struct ompHandle_st {
   bool profile = false;
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> ev_pool;
+  // CUDA graphs of recent batches' launch sequences (small LRU: callers that alternate output
+  // buffers, e.g. a fresh allocation per call under the caching allocator, still hit)
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    GraphKey key{};
+    int64_t launches = 0;
+    uint64_t used = 0;
+  };
+  static constexpr int kGraphCache = 4;
+  GraphEntry graphs[kGraphCache];
+  uint64_t graph_tick = 0;
+  bool graph_broken = false;
   double prof_ms[OMP_NUM_KERNEL_SLOTS] = {0};
   int64_t prof_n[OMP_NUM_KERNEL_SLOTS] = {0};
 };
@@ -171,6 +197,13 @@ struct Launcher {
   }
 };
 
+static void invalidate_graph(ompHandle_t h) {
+  for (auto& g : h->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = ompHandle_st::GraphEntry{};
+  }
+}
+
 static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   if (B <= h->capB && S <= h->capS) return OMP_OK;
   const int64_t nB = B > h->capB ? B : h->capB;
@@ -199,12 +232,14 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   h->capS = nS;
   h->ldf = ldf;
   h->ldu = nS;
+  invalidate_graph(h);               // the captured launches hold the old workspace pointers
   return OMP_OK;
 }
 
-static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
-                             float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
-                             float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
+// The launch sequence of one batch (also what gets captured into the CUDA graph).
+static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
+                                 float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
+                                 float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   ompStatus_t s = ensure_workspace(h, B, S);
   if (s != OMP_OK) return s;
   if (!(eps >= 0.f)) eps = -1.f;   // NaN or negative: no tolerance
@@ -269,6 +304,62 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
   return OMP_OK;
 }
 
+// One batch: the S-iteration launch sequence is captured once into a CUDA graph per (shape, eps,
+// buffers) and replayed on the caller's stream, so a batch costs one graph launch instead of
+// 1 + 2S (3S in SIMT mode) kernel launches (small-batch latency, §8(f) NEXT #3).
+// Profiling mode and OMP_B200_GRAPH=0 launch directly; a failed capture falls back to direct launch.
+static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
+                             float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
+                             float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
+  ompStatus_t s = ensure_workspace(h, B, S);   // allocations happen outside any capture
+  if (s != OMP_OK) return s;
+  static int env_graph = -1;
+  if (env_graph < 0) {
+    const char* e = getenv("OMP_B200_GRAPH");
+    env_graph = (e && e[0] == '0') ? 0 : 1;
+  }
+  // profiling brackets every kernel with events: launch directly (event nodes in a graph cost more)
+  if (h->profile || !env_graph || h->graph_broken)
+    return enqueue_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st);
+  const GraphKey key{B, ldy, ldx, lds, S, eps, Y, X, support, resid, n_iter, status};
+  ompHandle_st::GraphEntry* hit = nullptr;
+  for (auto& g : h->graphs)
+    if (g.exec && g.key == key) hit = &g;
+  if (!hit) {
+    hit = &h->graphs[0];                    // evict an empty or the least recently used entry
+    for (auto& g : h->graphs)
+      if (!g.exec || g.used < hit->used) hit = &g;
+    if (hit->exec) cudaGraphExecDestroy(hit->exec);
+    *hit = ompHandle_st::GraphEntry{};
+    if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_fail(h, cudaGetLastError());
+    // capture only records the launches; the replay is ordered on the caller's stream
+    cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    s = enqueue_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, h->cap_stream);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (s == OMP_OK && e == cudaSuccess) e = cudaGraphInstantiate(&hit->exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (s != OMP_OK || e != cudaSuccess) {
+      cudaGetLastError();
+      hit->exec = nullptr;
+      h->graph_broken = true;               // never try again on this handle; launch directly
+      if (s != OMP_OK && s != OMP_ERR_CUDA) return s;
+      return enqueue_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st);
+    }
+    hit->key = key;
+    hit->launches = h->last_launches;
+  }
+  hit->used = ++h->graph_tick;
+  cudaError_t e = cudaGraphLaunch(hit->exec, st);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  h->last_launches = hit->launches;
+  h->lastB = B;
+  h->lastS = S;
+  return OMP_OK;
+}
+
 static ompStatus_t check_batch_args(ompHandle_t h, const void* Y, int64_t B, int64_t ldy, int32_t S,
                                     const void* X, int64_t ldx, const void* support, int64_t lds,
                                     const void* resid, const void* n_iter, const void* status) {
@@ -307,6 +398,8 @@ ompStatus_t ompDestroy(ompHandle_t h) {
   {
     DevGuard g(h->device);
     cudaDeviceSynchronize();
+    invalidate_graph(h);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->norm); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
@@ -478,6 +571,7 @@ ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, 
   ompStatus_t s = ensure_workspace(h, B, h->capS > 0 ? h->capS : 1);
   if (s != OMP_OK) return s;
   if (B > h->capC) {
+    invalidate_graph(h);             // SIMT-mode graphs hold the old C
     if (!dalloc(h->C, (size_t)B * h->Np)) {
       h->capC = 0;
       return OMP_ERR_NOMEM;

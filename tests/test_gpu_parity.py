@@ -198,6 +198,37 @@ def test_batch_invariance_bitwise(mode):
         assert np.array_equal(full[key][130:260], part[key]), key
 
 
+def _fields(r):
+    return [t.cpu().numpy() for t in (r.X, r.support, r.resid_norm, r.n_iter, r.status)]
+
+
+@pytest.mark.parametrize("mode", ["bf16", "simt"])
+def test_graph_replay_matches_direct_launch(mode):
+    """The CUDA-graph replay (default path) equals direct launches (profiling mode) bit for bit,
+    across graph-cache hits, misses (fresh output buffers, new eps, new B) and evictions."""
+    import torch
+    from paper_2407_06434_b200 import OMP
+    prob = make_problem("c2", B=300)
+    Y = torch.from_numpy(prob.Y).cuda()
+    with OMP(torch.from_numpy(prob.A).cuda(), mode=mode) as h:
+        h.profile(True)
+        want = {}
+        for B, eps in [(300, None), (300, 0.3), (77, None)]:
+            r = h.batch(Y[:B], prob.S, eps)
+            want[(B, eps)] = _fields(r)
+        h.profile(False)
+        for rep in range(3):
+            for (B, eps), w in want.items():
+                r = h.batch(Y[:B], prob.S, eps)   # fresh outputs each call
+                got = _fields(r)
+                for a, b in zip(got, w):
+                    assert np.array_equal(a, b), (rep, B, eps)
+        assert h.launch_count() == 1 + (3 if mode == "simt" else 2) * prob.S
+        for _ in range(6):                        # > cache size distinct keys: eviction path
+            outs = h.batch(Y[:300], prob.S)
+        assert np.array_equal(outs.support.cpu().numpy(), want[(300, None)][1])
+
+
 def test_host_path_matches_device_path():
     import torch
     from paper_2407_06434_b200 import OMP
