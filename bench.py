@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for single-GPU testing")
+    p.add_argument("--small-limit", type=int, default=-1,
+                   help="small-batch persistent-kernel limit (-1 library default, 0 never)")
     p.add_argument("--no-kernel-profile", action="store_true",
                    help="time the steps through the CUDA-graph path without per-kernel events; the kernel "
                         "split then comes from one extra profiled step (small-batch latency runs)")
@@ -122,6 +124,15 @@ def measured_peaks():
         return None
 
 
+def l2_peak():
+    """Measured L2 gather bandwidth of this GPU model (scripts/l2_probe.cu, committed result)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "l2_probe_b200.json")))
+        return float(d["l2_gather_sustained_gbs"]), "profiles/l2_probe_b200.json l2_gather_sustained_gbs"
+    except Exception:
+        return 20500.0, "fallback 20.5 TB/s (scripts/l2_probe.cu on B200)"
+
+
 def ncu_traffic(kernel_key: str, config_name: str):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
     try:
@@ -153,8 +164,12 @@ def kernel_work(cfg, B, mode):
         "correlation": ("tensor", 2.0 * M * N * B, "TFLOP/s", None),
         # standalone argmax over the FP32 C (SIMT mode): 4N bytes per signal
         "select": ("hbm", B * 4.0 * N, "GB/s", None),
-        "update": ("hbm", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
+        "update": ("l2", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
         "init": ("hbm", B * (4.0 * M + (4.0 + planes) * Mp), "GB/s", None),
+        # small-batch persistent kernel, all S iterations: per iteration the atom table once (phase A,
+        # exact correlation over all N atoms) + the per-signal append/residual bytes (L2-resident)
+        "small": ("l2", S * (4.0 * N * Mp + B * (4.0 * Mp * (k + 3) + 4.0 * k * (k + 1) / 2 + 4.0 * M)), "GB/s",
+                  {"hbm_bytes": B * 4.0 * (M + S + S * (S + 1) / 2), "l2_gather_bytes": S * (4.0 * N * Mp + B * 4.0 * Mp * (k + 3))}),
     }
 
 
@@ -196,6 +211,8 @@ def main():
     eps32 = None if eps is None else float(np.float32(eps))
 
     h = OMP(A, mode=args.mode)
+    if args.small_limit != -1:
+        h.set_small_batch_limit(args.small_limit)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -288,6 +305,15 @@ def main():
             peak = base / 2.0 / (3.0 if args.mode == "3xtf32" else 1.0) if args.mode != "simt" else 74.0
             peak_src = "bf16 sustained x nominal tf32/bf16 ratio 1/2 (/3 for 3 products)" if args.mode != "simt" \
                 else "FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz"
+    elif bound == "l2":
+        # the update kernel's bytes all pass through L2 (the atom-row gather hits it; the streamed rows
+        # come from HBM through it): its roof is the L2 read bandwidth measured on a B200 by
+        # scripts/l2_probe.cu with the kernel's own access pattern (profiles/l2_probe_b200.json)
+        achieved = per_launch / t_launch / 1e9
+        peak, peak_src = l2_peak()
+        roofline_extra = {"hbm_bytes": split["hbm_bytes"], "l2_gather_bytes": split["l2_gather_bytes"],
+                          "hbm_floor_ms": split["hbm_bytes"] / ((peaks or {}).get("hbm_gbs", 6650.0) * 1e6),
+                          "l2_floor_ms": per_launch / (peak * 1e6)}
     else:
         achieved = per_launch / t_launch / 1e9
         peak = (peaks or {}).get("hbm_gbs", 6650.0)
@@ -295,22 +321,21 @@ def main():
     roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": achieved / peak, "traffic": ncu_traffic(dom, args.config), "peak_source": peak_src,
                 "work_per_launch": per_launch, "launch_ms": t_launch * 1e3}
-    if split:
-        # the update kernel's atom gather is served by L2: report the effective-bandwidth split and the
-        # L2 roofline: ncu lts__t_sectors peak = 3 sectors/clk x 184 slices x 32 B x 1.958 GHz
-        l2_peak = 34600.0
-        roofline.update({"hbm_bytes": split["hbm_bytes"], "l2_gather_bytes": split["l2_gather_bytes"],
-                         "effective": "achieved = (streamed HBM bytes + L2 gather bytes) / launch time",
-                         "l2_peak_gbs": l2_peak, "frac_of_l2_peak": achieved / l2_peak})
+    if bound == "l2":
+        roofline.update(roofline_extra)
     other = {k: kern[k] for k in kern if k in work and k != dom and kern[k][1] > 0}
     roofline["others"] = {}
     for k, (tot_ms, n_l) in other.items():
         b2, w2, u2, _ = work[k]
         t2 = tot_ms / n_l / 1e3
         if b2 == "tensor":
-            roofline["others"][k] = {"achieved_tflops": w2 / t2 / 1e12, "launch_ms": t2 * 1e3}
+            tp = (peaks or {}).get("bf16_tflops_sustained", 1400.0) if args.mode == "bf16" else None
+            roofline["others"][k] = {"bound": b2, "achieved_tflops": w2 / t2 / 1e12, "launch_ms": t2 * 1e3,
+                                     "frac": (w2 / t2 / 1e12 / tp) if tp else None}
         else:
-            roofline["others"][k] = {"achieved_gbs": w2 / t2 / 1e9, "launch_ms": t2 * 1e3}
+            bp = l2_peak()[0] if b2 == "l2" else (peaks or {}).get("hbm_gbs", 6650.0)
+            roofline["others"][k] = {"bound": b2, "achieved_gbs": w2 / t2 / 1e9, "launch_ms": t2 * 1e3,
+                                     "frac": w2 / t2 / 1e9 / bp}
     kernels = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / max(1e-9, sum(x[0] for x in kern.values()))}
                for k, v in kern.items()}
 

@@ -136,12 +136,23 @@ ompStatus_t ompGetFactor(ompHandle_t handle, int64_t b0, int64_t count, float* F
 
 /* Profiling: when enabled, ompBatch brackets every kernel with CUDA events on `stream`;
  * ompProfileRead returns, per kernel slot (0 init, 1 correlation, 2 standalone argmax [SIMT
- * mode], 3 update = exact selection + factor append + residual, 4 reserved), the summed
+ * mode], 3 update = exact selection + factor append + residual, 4 small-batch persistent
+ * kernel = all S iterations of a small batch in one launch), the summed
  * milliseconds and the number of launches since the last reset.  Reading synchronises the
  * events.                                                                                  */
 #define OMP_NUM_KERNEL_SLOTS 5
 ompStatus_t ompProfileEnable(ompHandle_t handle, int enable);
 ompStatus_t ompProfileRead(ompHandle_t handle, double* ms, int64_t* launches, int reset);
+
+/* ompSetSmallBatchLimit — batches of at most `max_batch` signals run on the small-batch path:
+ *   one persistent cooperative kernel for all S iterations (exact FP32 correlation over all N
+ *   atoms, then factor append + residual per signal, PAPER.md:243 on
+ *   per-call overhead at small batch sizes) instead of 1 + 2S launches.  Results are bitwise
+ *   identical to the screened path's.  max_batch = -1 (default): automatic (B <= 8 and
+ *   B * N * Mp <= 2^26, the measured crossover); 0: never; else B <= max_batch (<= 64).  Tensor-core correlation modes only (SIMT mode keeps its own argmax);
+ *   the path also needs Mp <= 2048 and B x Mp x 4 bytes of shared memory (<= 150 KB), else the
+ *   screened path runs.  OMP_ERR_INVALID_ARG for max_batch < -1.                           */
+ompStatus_t ompSetSmallBatchLimit(ompHandle_t handle, int64_t max_batch);
 
 /* Kernel launches issued by the last ompBatch (for launch accounting).                   */
 int64_t ompGetLaunchCount(ompHandle_t handle);

@@ -13,7 +13,8 @@ import os
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_void_p, c_char_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libomp_b200.so")
+# OMP_B200_LIB: load another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("OMP_B200_LIB") or os.path.join(HERE, "libomp_b200.so")
 
 OMP_OK = 0
 OMP_ERR_INVALID_ARG = 1
@@ -32,7 +33,7 @@ OMP_CORR_BF16 = 0
 OMP_CORR_FP32_SIMT = 1
 OMP_CORR_3XTF32 = 2
 OMP_NUM_KERNEL_SLOTS = 5
-KERNEL_SLOTS = ("init", "correlation", "select", "update", "reserved")
+KERNEL_SLOTS = ("init", "correlation", "select", "update", "small")
 
 # name -> (restype, argtypes); the list is also the ABI inventory tests check against the header
 SIGNATURES = {
@@ -49,6 +50,7 @@ SIGNATURES = {
     "ompProfileEnable": (c_int, [c_void_p, c_int]),
     "ompProfileRead": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), c_int]),
     "ompGetLaunchCount": (c_int64, [c_void_p]),
+    "ompSetSmallBatchLimit": (c_int, [c_void_p, c_int64]),
     "ompDestroy": (c_int, [c_void_p]),
     "ompGetErrorString": (c_char_p, [c_int]),
     "ompGetErrorDetail": (c_int64, [c_void_p]),
@@ -70,6 +72,8 @@ def load(path: str = LIB_PATH):
             "(there is no CPU or eager fallback)")
     lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("OMP_B200_LIB") and not hasattr(lib, name):
+            continue                    # an older build under A/B test: only its own entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -141,10 +141,14 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
     status[b] = st;
     s_slot = -1;
     if (st == SIG_RUNNING) {
-      s_slot = atomicAdd(live0, 1);
-      rslot[s_slot] = rn;
+      if (live0) {
+        s_slot = atomicAdd(live0, 1);
+        rslot[s_slot] = rn;
+      } else {
+        s_slot = (int)b;                  // small-batch path: no compaction
+      }
     }
-    slot[b] = s_slot;
+    if (slot) slot[b] = s_slot;
   }
   __syncthreads();
   const int sl = s_slot;

@@ -66,6 +66,10 @@ struct ompHandle_st {
   float* cstar = nullptr;
   float2* part = nullptr;   // screening epilogue: (B) x (Np / 128) x TOPK candidates
   int64_t capC = 0;         // rows of C (SIMT mode / ompCorrelate)
+  // small-batch path (k_small.cu): partials (SMALL_MAX_B x SMs x SMALL_MAX_CTAS_PER_SM) + barrier
+  int64_t small_limit = -1; // -1 automatic, 0 never, > 0 explicit maximum batch
+  float4* pbest = nullptr;
+  unsigned int* gbar = nullptr;
   int64_t ldf = 0, ldu = 0;
   int64_t lastB = 0;
   int32_t lastS = 0;
@@ -236,14 +240,64 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   return OMP_OK;
 }
 
+// Does a batch of B run on the small-batch persistent kernel?  Automatic rule, from the measured
+// crossover on B200 (the persistent kernel wins below B ~ 6..12 on c2..c5): B <= 8
+// and its exact correlation (B N Mp FMAs per iteration, phase A of k_small.cu) within 2^26.
+static bool use_small(ompHandle_t h, int64_t B, int32_t S) {
+  if (!tc_mode(h) || h->small_limit == 0 || !small_path_supported(B, h->Mp, S)) return false;
+  if (h->small_limit > 0) return B <= h->small_limit;
+  return B <= 8 && (double)B * (double)h->N * (double)h->Mp <= 67108864.0;
+}
+
+static ompStatus_t ensure_small(ompHandle_t h) {
+  if (h->pbest) return OMP_OK;
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  if (!dalloc(h->pbest, (size_t)SMALL_MAX_B * sms * SMALL_MAX_CTAS_PER_SM) || !dalloc(h->gbar, 1)) {
+    dfree(h->pbest);
+    dfree(h->gbar);
+    cudaGetLastError();
+    return OMP_ERR_NOMEM;
+  }
+  return OMP_OK;
+}
+
 // The launch sequence of one batch (also what gets captured into the CUDA graph).
 static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
                                  float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
                                  float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   ompStatus_t s = ensure_workspace(h, B, S);
   if (s != OMP_OK) return s;
-  if (!(eps >= 0.f)) eps = -1.f;   // NaN or negative: no tolerance
   Launcher L{h, st};
+  if (!(eps >= 0.f)) eps = -1.f;   // NaN or negative: no tolerance
+  if (use_small(h, B, S)) {
+    // small-batch path: init (rows = signals, no compaction) + one persistent kernel
+    s = ensure_small(h);
+    if (s != OMP_OK) return s;
+    cudaError_t e = cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(0);
+    e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, r32_buf(h, 0), nullptr, nullptr, nullptr, X, ldx, support,
+                          lds, resid, n_iter, status, nullptr, nullptr, nullptr, st);
+    L.end(0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    UpdateLaunch U = {};
+    U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
+    U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
+    U.Y = Y; U.ldy = ldy; U.F = h->F; U.ldf = h->ldf; U.U = h->U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
+    U.support = support; U.lds = lds; U.R32 = r32_buf(h, 0);
+    U.resid = resid; U.n_iter = n_iter; U.status = status;
+    L.begin(4);
+    e = launch_small(U, h->pbest, h->gbar, st);
+    L.end(4);
+    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    h->last_launches = L.count;
+    h->lastB = B;
+    h->lastS = S;
+    return OMP_OK;
+  }
   cudaError_t e = cudaMemsetAsync(h->live, 0, sizeof(int32_t) * ((size_t)S + 2), st);
   if (e != cudaSuccess) return cuda_fail(h, e);
   L.begin(0);
@@ -312,6 +366,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
                              float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
                              float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   ompStatus_t s = ensure_workspace(h, B, S);   // allocations happen outside any capture
+  if (s == OMP_OK && use_small(h, B, S)) s = ensure_small(h);
   if (s != OMP_OK) return s;
   static int env_graph = -1;
   if (env_graph < 0) {
@@ -393,6 +448,13 @@ int64_t ompGetErrorDetail(ompHandle_t h) { return h ? h->err_detail : g_create_d
 
 int64_t ompGetLaunchCount(ompHandle_t h) { return h ? h->last_launches : 0; }
 
+ompStatus_t ompSetSmallBatchLimit(ompHandle_t h, int64_t max_batch) {
+  if (!h || max_batch < -1) return OMP_ERR_INVALID_ARG;
+  if (h->small_limit != max_batch) invalidate_graph(h);   // cached graphs hold the other path
+  h->small_limit = max_batch;
+  return OMP_OK;
+}
+
 ompStatus_t ompDestroy(ompHandle_t h) {
   if (!h) return OMP_ERR_INVALID_ARG;
   {
@@ -402,6 +464,8 @@ ompStatus_t ompDestroy(ompHandle_t h) {
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->norm); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
+    dfree(h->pbest);
+    dfree(h->gbar);
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
     dfree(h->rslot); dfree(h->slot); dfree(h->live);
     dfree(h->nstar); dfree(h->cstar); dfree(h->part);

@@ -68,7 +68,8 @@ cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t l
 cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp, float* R32,
                                void* Rb, float* R_hi, float* R_lo, cudaStream_t st);
 // a1: batch init; running signals take live-set slots (atomic counter *live0) and their r_0 = y
-// planes go to row slot[b]; rslot[slot] = ||y||
+// planes go to row slot[b]; rslot[slot] = ||y||.  live0 == nullptr: no compaction, row b (slot and
+// rslot may then be null).
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
@@ -112,6 +113,14 @@ struct UpdateLaunch {
   size_t l2_persist_bytes;  // > 0: launch with a persisting L2 access-policy window over At
 };
 cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st);
+// ---- small-batch path: all S iterations in one persistent cooperative kernel (k_small.cu) ----
+constexpr int SMALL_MAX_B = 64;            // largest batch the persistent kernel takes
+constexpr int SMALL_MAX_CTAS_PER_SM = 8;   // pbest holds SMALL_MAX_B x (SMs x this) partials
+bool small_path_supported(int64_t B, int64_t Mp, int32_t S);
+// L as for launch_update (k, part, nstar, cstar, R32in, Rb/Rhi/Rlo, rslot_out, slot, live_next unused);
+// L.R32 = the residual rows at row b, initialised by launch_batch_init with live0 = nullptr.
+// pbest: SMALL_MAX_B x SMs x SMALL_MAX_CTAS_PER_SM float4; bar: one counter, zero at launch.
+cudaError_t launch_small(const UpdateLaunch& L, float4* pbest, unsigned int* bar, cudaStream_t st);
 cudaError_t launch_densify(const float* X, int64_t ldx, const int32_t* support, int64_t lds,
                            const int32_t* n_iter, int64_t B, int32_t S, int64_t N, float* Xd,
                            int64_t ldxd, cudaStream_t st);

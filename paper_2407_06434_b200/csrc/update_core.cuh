@@ -1,0 +1,467 @@
+// Device code shared by the per-iteration update kernel (k_update.cu) and the small-batch
+// persistent kernel (k_small.cu): the exact FP32 correlation dot, and the per-signal tail of one
+// OMP iteration once the atom n* and its correlation c* are known:
+//
+//  a4  inverse-Cholesky factor append, the paper's algorithm-v0 update:
+//        w = A_k^T a_{n*} = [A^T A]_{n*, S_k}
+//        z = F_k^T w,  gamma = 1/sqrt(||a_{n*}||^2 - ||z||^2)
+//        F_{k+1} = [[F_k, -gamma F_k z], [0, gamma]]                               (Eq. 8)
+//        u = F^T A^T y grows by u_new = gamma <r_k, a_{n*}> = gamma c*  (q = A_{k+1} f is orthogonal
+//            to span A_k, so q^T y = q^T r_k; pin P9)
+//        x = F_{k+1} u   (matrix-vector products only, Eq. 11)
+//      F is upper triangular, packed by columns (column j = F[0..j, j] at offset j(j+1)/2), the
+//      paper's packed representation.
+//
+//  a5  residual r_b = y_b - sum_{j<=k} x_j a_{s_j} from gathered atom rows of A^T,
+//      ||r_b||, the eps test, and the operand planes of the next screen.
+//
+// Both kernels run the same instructions in the same order for a signal, so a signal's result does
+// not depend on which kernel (i.e. which batch size) processed it.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "omp_internal.cuh"
+
+// optional timeline hook (k_small.cu defines it for its diagnostic trace; a no-op elsewhere)
+#ifndef OMP_TAIL_TRACE
+#define OMP_TAIL_TRACE(p)
+#endif
+
+namespace ompb {
+
+struct UpdateArgs {
+  int32_t k, S;
+  float eps;
+  int64_t N, M, Mp;
+  // selection inputs
+  const float2* part;   // screen partials (REFINE)
+  int groups;           // screen partial groups per row (Np / SCREEN_GROUP)
+  float window;
+  const int32_t* nstar; // preselected (SIMT mode)
+  const float* cstar;
+  // dictionary
+  const float* At;      // fp32 atom rows (Np x Mp)
+  const float* inv_norm;
+  const float* G;       // Gram matrix, row stride ldg
+  int64_t ldg;
+  // per-signal state
+  const float* Y;
+  int64_t ldy;
+  float* F;
+  int64_t ldf;
+  float* U;
+  int64_t ldu;
+  float* X;
+  int64_t ldx;
+  int32_t* support;
+  int64_t lds;
+  const float* R32in;   // current residual rows (row = slot)
+  float* R32;           // next residual planes (row = new slot)
+  __nv_bfloat16* Rb;
+  float* Rhi;
+  float* Rlo;
+  float* rslot_out;
+  int32_t* slot;
+  int32_t* live_next;   // nullptr: no live-set compaction, the signal keeps row b
+  float* resid;
+  int32_t* n_iter;
+  int32_t* status;
+};
+
+struct Cand {
+  float w;
+  int n;
+  float c;
+};
+
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {   // is a better than b
+  return a.w > b.w || (a.w == b.w && a.n < b.n);
+}
+
+__device__ __forceinline__ float tf32_rna_u(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// L2 policies: the 64 MB (c4) fp32 atom table is re-read by every signal and should stay in L2;
+// y, the residual planes and the factors are streamed once per iteration.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg_policy(const float4* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_policy(float4* ptr, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+               ::"l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_policy(uint2* ptr, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
+               ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+template <int T>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = 0.f;
+#pragma unroll
+  for (int w = 0; w < T / 32; ++w) r += red[w];
+  return r;
+}
+
+// one float4 chunk into a partial sum, in the fixed order w, z, y, x
+__device__ __forceinline__ float fma4(const float4 r, const float4 a, float s) {
+  return fmaf(r.x, a.x, fmaf(r.y, a.y, fmaf(r.z, a.z, fmaf(r.w, a.w, s))));
+}
+
+// The exact FP32 correlation c = <r, a_n> of one warp, in one fixed order: lane l owns the float4
+// chunks q = l + 32 i; chunk i goes to partial sum i mod 4 while a whole group of four exists, the
+// rest to partial 0; then (s0 + s1) + (s2 + s3) and an xor tree over the lanes.  The selection in both
+// update paths uses this order (warp_dot and warp_dot_regs below), so they agree bit for bit.
+__device__ __forceinline__ float warp_dot(const float4* __restrict__ r4, const float4* __restrict__ a4, int q4,
+                                          int lane) {
+  // four float4 loads in flight per lane, four partial sums
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int q = lane;
+  for (; q + 96 < q4; q += 128) {
+    const float4 a0 = __ldg(a4 + q), a1 = __ldg(a4 + q + 32), a2 = __ldg(a4 + q + 64), a3 = __ldg(a4 + q + 96);
+    const float4 r0 = r4[q], r1 = r4[q + 32], r2 = r4[q + 64], r3 = r4[q + 96];
+    s0 = fma4(r0, a0, s0);
+    s1 = fma4(r1, a1, s1);
+    s2 = fma4(r2, a2, s2);
+    s3 = fma4(r3, a3, s3);
+  }
+  for (; q < q4; q += 32) s0 = fma4(r4[q], __ldg(a4 + q), s0);
+  float acc = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// the same dot with the atom's chunks held in registers (areg[i] = chunk lane + 32 i, KC >= chunks)
+template <int KC>
+__device__ __forceinline__ float warp_dot_regs(const float4* __restrict__ r4, const float4 (&areg)[KC], int q4,
+                                               int lane) {
+  static_assert(KC % 4 == 0, "KC: groups of four chunks");
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int i = 0; i < KC; i += 4) {
+    const int q = lane + 32 * i;
+    if (q + 96 < q4) {
+      s0 = fma4(r4[q], areg[i], s0);
+      s1 = fma4(r4[q + 32], areg[i + 1], s1);
+      s2 = fma4(r4[q + 64], areg[i + 2], s2);
+      s3 = fma4(r4[q + 96], areg[i + 3], s3);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (q + 32 * t < q4) s0 = fma4(r4[q + 32 * t], areg[i + t], s0);
+    }
+  }
+  float acc = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Per-signal scratch in shared memory for the tail (Sp >= k + 1 entries each).
+struct TailSmem {
+  float *w, *z, *u, *xs;
+  int* ss;
+  uint32_t* ro;   // atom row offsets (float4 units) for the gather
+  float* red;     // T / 32 floats
+  int* bcast;     // one int
+};
+
+// a4 + a5 for signal b at iteration k with the selected atom n >= 0 and c* = <r_k, a_n>.
+// P: atom rows in flight per thread in the gather, ZC: columns per warp in z = F^T w (the
+// per-iteration kernel hides latency with 8 CTAs per SM and uses 2 / 2; the persistent small-batch
+// kernel has one CTA per signal on the critical path and uses more).  Neither changes the order of
+// any floating-point operation, only how far loads and reductions run ahead.
+// Preconditions: sm.ss[0..k) = support, sm.u[0..k) = u, visible to every thread.  Every exit is
+// uniform over the CTA.  Fb: the packed F_k (global memory, prefetched into L1, or a shared-memory
+// copy); Fs_append (nullable): a shared-memory copy that receives the new column as well.  On
+// return sm.ss[k] = n* and sm.u[k] = u_new, so a persistent caller's copies stay current.
+// rows_sm (nullable): a shared-memory copy of the support's atom rows (row j at rows_sm + j q4,
+// j <= k; row k may still be landing by cp.async, waited for here) that the gather reads instead
+// of A^T in global memory -- the same values, so the same result.
+template <int T, int CH, int P = 2, int ZC = 2>
+__device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
+                                                const float cst, const TailSmem& sm, const float* Fb,
+                                                float* Fs_append, const float4* rows_sm = nullptr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q4 = (int)(a.Mp >> 2);
+  float* w = sm.w;
+  float* z = sm.z;
+  float* u = sm.u;
+  float* xs = sm.xs;
+  int* ss = sm.ss;
+  uint32_t* ro = sm.ro;
+
+  // ---- a4: factor append --------------------------------------------------------------------------
+  const float* grow = a.G + (int64_t)n * a.ldg;
+  const float d = grow[n];              // ||a_{n*}||^2 (issued with the w loads, used after z)
+  bool dup = false;
+  for (int j = tid; j < k; j += T) {
+    const int s = ss[j];
+    ro[j] = (uint32_t)s * (uint32_t)q4;
+    dup |= (s == n);
+    w[j] = grow[s];                     // [A^T A]_{n*, s_j}
+  }
+  if (__syncthreads_or(dup)) {          // re-selection (reading R6)
+    if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
+    return;
+  }
+  OMP_TAIL_TRACE(0);
+  // z_j = F[:, j] . w  (column dots: lane l sums i = l, l + 32, ... <= j, then an xor tree; a warp
+  // takes ZC columns at a time so their loads and shuffle reductions overlap -- ZC changes only the
+  // interleaving, not any column's arithmetic)
+  constexpr int NW = T / 32;
+  for (int j0 = ZC * warp; j0 < k; j0 += ZC * NW) {
+    const float* col[ZC];
+    float acc_z[ZC];
+#pragma unroll
+    for (int c = 0; c < ZC; ++c) {
+      col[c] = Fb + (int64_t)(j0 + c) * (j0 + c + 1) / 2;
+      acc_z[c] = 0.f;
+    }
+    const int jl = min(j0 + ZC, k) - 1;   // last column of the group
+    for (int i = lane; i <= jl; i += 32) {
+      const float wi = w[i];
+#pragma unroll
+      for (int c = 0; c < ZC; ++c)
+        if (i <= j0 + c && j0 + c < k) acc_z[c] = fmaf(col[c][i], wi, acc_z[c]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < ZC; ++c) acc_z[c] += __shfl_xor_sync(0xffffffffu, acc_z[c], o);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < ZC; ++c)
+        if (j0 + c < k) z[j0 + c] = acc_z[c];
+  }
+  __syncthreads();
+  OMP_TAIL_TRACE(1);
+  float zz = 0.f;
+  for (int j = tid; j < k; j += T) zz = fmaf(z[j], z[j], zz);
+  zz = block_sum<T>(zz, sm.red);
+
+  OMP_TAIL_TRACE(2);
+  const float delta = d - zz;
+  if (!(delta > TAU_F * d)) {           // rank deficiency (reading R6); also catches NaN
+    if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
+    return;
+  }
+  const float gamma = 1.0f / sqrtf(delta);
+  const float unew = gamma * cst;       // gamma <r_k, a_{n*}>
+  // v = F_k z and t = F_k u in one pass over F (thread per row; lanes of a warp share column j)
+  float* newcol = a.F + b * a.ldf + (int64_t)k * (k + 1) / 2;
+  for (int i = tid; i < k; i += T) {
+    // four independent partial sums so four column loads are in flight per thread
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    int j = i & ~31;
+    int o = j * (j + 1) / 2 + i;                  // offset of F[i, j] in the packed columns
+    for (; j + 4 <= k; j += 4) {
+      const int o1 = o + j + 1, o2 = o1 + j + 2, o3 = o2 + j + 3;
+      const float f0 = (j >= i) ? Fb[o] : 0.f;
+      const float f1 = (j + 1 >= i) ? Fb[o1] : 0.f;
+      const float f2 = (j + 2 >= i) ? Fb[o2] : 0.f;
+      const float f3 = (j + 3 >= i) ? Fb[o3] : 0.f;
+      o = o3 + j + 4;
+      v0 = fmaf(f0, z[j], v0);
+      t0 = fmaf(f0, u[j], t0);
+      v1 = fmaf(f1, z[j + 1], v1);
+      t1 = fmaf(f1, u[j + 1], t1);
+      v2 = fmaf(f2, z[j + 2], v2);
+      t2 = fmaf(f2, u[j + 2], t2);
+      v3 = fmaf(f3, z[j + 3], v3);
+      t3 = fmaf(f3, u[j + 3], t3);
+    }
+    for (; j < k; ++j) {
+      const float f = (j >= i) ? Fb[o] : 0.f;
+      o += j + 1;
+      v0 = fmaf(f, z[j], v0);
+      t0 = fmaf(f, u[j], t0);
+    }
+    const float v = (v0 + v1) + (v2 + v3);
+    const float t = (t0 + t1) + (t2 + t3);
+    newcol[i] = -gamma * v;                       // -gamma F_k z
+    if (Fs_append) Fs_append[(int64_t)k * (k + 1) / 2 + i] = -gamma * v;
+    const float xi = fmaf(-gamma * v, unew, t);   // x_i = (F_k u)_i + f_i u_new
+    a.X[b * a.ldx + i] = xi;
+    xs[i] = xi;
+  }
+  if (tid == 0) {
+    newcol[k] = gamma;
+    if (Fs_append) Fs_append[(int64_t)k * (k + 1) / 2 + k] = gamma;
+    u[k] = unew;
+    const float xk = gamma * unew;
+    a.X[b * a.ldx + k] = xk;
+    xs[k] = xk;
+    ss[k] = n;
+    ro[k] = (uint32_t)n * (uint32_t)q4;
+    a.U[b * a.ldu + k] = unew;
+    a.support[b * a.lds + k] = n;
+  }
+  if (rows_sm) asm volatile("cp.async.wait_all;" ::: "memory");   // row k of the cache
+  __syncthreads();
+  OMP_TAIL_TRACE(3);
+
+  // ---- a5: residual r = y - A_S x, ||r||, eps test, next screening operand ------------------------
+  // L2-bandwidth bound gather: per atom pair, every thread issues its 2 x CH float4 loads before the
+  // FMAs; with T * CH == Mp / 4 (the benchmark shapes) no load is predicated.
+  const int kk = k + 1;
+  const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+  float4 acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* A4 = reinterpret_cast<const float4*>(a.At) + tid;
+  {
+    // chunk c of this thread exists for every row (T * CH == q4 at the benchmark shapes: no predicate)
+    bool has[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) has[c] = (T * CH == q4) || (tid + c * T < q4);
+    // fold x_j times row j into acc, j ascending; rows come P at a time (loads before FMAs)
+    const bool full = (T * CH == q4);
+    auto fold = [&](const float x, const float4 (&v)[CH]) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (full || has[c]) {
+          acc[c].x = fmaf(x, v[c].x, acc[c].x);
+          acc[c].y = fmaf(x, v[c].y, acc[c].y);
+          acc[c].z = fmaf(x, v[c].z, acc[c].z);
+          acc[c].w = fmaf(x, v[c].w, acc[c].w);
+        }
+      }
+    };
+    auto gather = [&](auto load_row) {
+      int j = 0;
+      for (; j + P <= kk; j += P) {
+        float4 v[P][CH];
+#pragma unroll
+        for (int p = 0; p < P; ++p) load_row(j + p, v[p]);
+#pragma unroll
+        for (int p = 0; p < P; ++p) fold(xs[j + p], v[p]);
+      }
+      for (; j < kk; ++j) {
+        float4 v[CH];
+        load_row(j, v);
+        fold(xs[j], v);
+      }
+    };
+    if (rows_sm) {
+      gather([&](int j, float4 (&v)[CH]) {
+        const float4* r = rows_sm + (size_t)j * q4 + tid;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) v[c] = has[c] ? r[c * T] : make_float4(0.f, 0.f, 0.f, 0.f);
+      });
+    } else if (full) {           // every chunk exists: unpredicated loads
+      gather([&](int j, float4 (&v)[CH]) {
+        const float4* r = A4 + ro[j];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) v[c] = ldg_policy(r + c * T, keep);
+      });
+    } else {
+      gather([&](int j, float4 (&v)[CH]) {
+        const float4* r = A4 + ro[j];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) v[c] = has[c] ? ldg_policy(r + c * T, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+      });
+    }
+  }
+  OMP_TAIL_TRACE(4);
+  const float* y = a.Y + b * a.ldy;
+  const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
+  float part = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int q = tid + c * T;
+    if (q < q4) {
+      const int64_t m = (int64_t)q << 2;
+      float4 yv;
+      if (yvec && m + 3 < a.M) {
+        yv = ldg_policy(reinterpret_cast<const float4*>(y + m), stream);
+      } else {
+        yv.x = m < a.M ? y[m] : 0.f;
+        yv.y = m + 1 < a.M ? y[m + 1] : 0.f;
+        yv.z = m + 2 < a.M ? y[m + 2] : 0.f;
+        yv.w = m + 3 < a.M ? y[m + 3] : 0.f;
+      }
+      acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);   // r
+      part = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, fmaf(acc[c].w, acc[c].w, part))));
+    }
+  }
+  const float rr = block_sum<T>(part, sm.red);
+  OMP_TAIL_TRACE(5);
+  if (tid == 0) {
+    const float rn = sqrtf(rr);
+    a.resid[b] = rn;
+    a.n_iter[b] = kk;
+    int ns = -1;
+    if (a.eps >= 0.f && rn <= a.eps) a.status[b] = OMP_SIG_EPS;
+    else if (kk == a.S) a.status[b] = OMP_SIG_MAXITER;
+    else if (a.live_next) {
+      ns = atomicAdd(a.live_next, 1);                                  // next live-set slot
+      a.rslot_out[ns] = rn;
+    } else {
+      ns = (int)b;                                                     // no compaction: row b
+    }
+    if (a.slot) a.slot[b] = ns;
+    *sm.bcast = ns;
+  }
+  __syncthreads();
+  const int ns = *sm.bcast;
+  if (ns < 0) return;                   // finished: no planes for the next screen
+  const int64_t ro_out = (int64_t)ns * a.Mp;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int q = tid + c * T;
+    if (q < q4) {
+      const float4 r = acc[c];
+      if (a.R32) stg_policy(reinterpret_cast<float4*>(a.R32 + ro_out) + q, r, stream);
+      if (a.Rb) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(r.x, r.y), p1 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&p0);
+        pk.y = *reinterpret_cast<uint32_t*>(&p1);
+        stg_policy(reinterpret_cast<uint2*>(a.Rb + ro_out) + q, pk, stream);
+      }
+      if (a.Rhi) {
+        const float4 h = make_float4(tf32_rna_u(r.x), tf32_rna_u(r.y), tf32_rna_u(r.z), tf32_rna_u(r.w));
+        reinterpret_cast<float4*>(a.Rhi + ro_out)[q] = h;
+        reinterpret_cast<float4*>(a.Rlo + ro_out)[q] = make_float4(r.x - h.x, r.y - h.y, r.z - h.z, r.w - h.w);
+      }
+    }
+  }
+}
+
+}  // namespace ompb

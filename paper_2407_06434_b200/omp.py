@@ -165,6 +165,10 @@ class OMP:
         check(self.lib.ompProfileRead(self.handle, ms, n, int(reset)), "ompProfileRead", self.handle)
         return {name: (ms[i], n[i]) for i, name in enumerate(_lib.KERNEL_SLOTS)}
 
+    def set_small_batch_limit(self, max_batch: int):
+        """-1 automatic (default), 0 never, else the largest batch run by the persistent kernel."""
+        check(self.lib.ompSetSmallBatchLimit(self.handle, int(max_batch)), "ompSetSmallBatchLimit", self.handle)
+
     def launch_count(self) -> int:
         return int(self.lib.ompGetLaunchCount(self.handle))
 

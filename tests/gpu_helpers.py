@@ -14,14 +14,24 @@ def eps32(eps):
     return None if eps is None else float(np.float32(eps))
 
 
+# test "modes": the library's correlation modes on the screened (per-iteration) path, plus "small":
+# the small-batch persistent kernel (bf16 handle, small-batch limit 64; larger batches fall back to
+# the screened path)
+PATHS = {"bf16": ("bf16", 0), "3xtf32": ("3xtf32", 0), "simt": ("simt", 0), "small": ("bf16", 64),
+         "auto": ("bf16", -1)}   # "auto": the library default (what bench.py and users run)
+
+
 def run_gpu(A_np, Y_np, S, eps=None, mode="bf16", handle=None):
     import torch
     from paper_2407_06434_b200 import OMP
     A = torch.from_numpy(A_np).cuda()
     Y = torch.from_numpy(np.ascontiguousarray(Y_np)).cuda()
     own = handle is None
-    h = OMP(A, mode=mode) if own else handle
+    lib_mode, small = PATHS[mode]
+    h = OMP(A, mode=lib_mode) if own else handle
     try:
+        if own:
+            h.set_small_batch_limit(small)
         res = h.batch(Y, S, eps32(eps))
         torch.cuda.synchronize()
         out = dict(support=res.support.cpu().numpy(), X=res.X.cpu().numpy(),

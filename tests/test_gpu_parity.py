@@ -16,7 +16,8 @@ from oracle import DEGENERATE, EPS, MAXITER, NAN
 from synth import make_dictionary, make_problem, make_signals
 
 pytestmark = pytest.mark.gpu
-MODES = ["bf16", "3xtf32", "simt"]
+MODES = ["bf16", "3xtf32", "simt", "small"]    # gpu_helpers.PATHS; "small" = persistent kernel
+LIB_MODES = ["bf16", "3xtf32", "simt"]
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
 
@@ -34,7 +35,7 @@ def screening_bound(mode, K):
     return 1e-6
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", LIB_MODES)
 @pytest.mark.parametrize("shape", [(32, 64, 16), (256, 1024, 1000), (300, 700, 333), (1024, 4096, 520),
                                    (2048, 8192, 1024)])
 def test_correlation_gemm_vs_fp64(mode, shape):
@@ -89,10 +90,11 @@ def test_parity_tiny(mode):
     rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, range(prob.B))
     d = assert_no_bugs(rep, f"tiny/{mode}")
     assert d["counts"].get("exact", 0) == prob.B
-    assert out["launches"] == 1 + (3 if mode == "simt" else 2) * prob.S   # init + per-iteration kernels
+    # init + per-iteration kernels, or init + the persistent kernel
+    assert out["launches"] == (2 if mode == "small" else 1 + (3 if mode == "simt" else 2) * prob.S)
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", LIB_MODES)
 def test_parity_c2_all(mode):
     prob = make_problem("c2")
     out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
@@ -101,7 +103,7 @@ def test_parity_c2_all(mode):
     assert d["counts"].get("exact", 0) + d["counts"].get("flagged_ok", 0) >= 995
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", LIB_MODES)
 def test_parity_c3_full_batch_sampled(mode):
     prob = make_problem("c3", device="cuda")
     out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
@@ -115,7 +117,7 @@ def test_parity_c3_full_batch_sampled(mode):
 @pytest.mark.parametrize("B", [1, 10, 1000, 100000])
 def test_parity_c5_sweep_sampled(B):
     prob = make_problem("c5", B=B, device="cuda" if B > 1000 else None)
-    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "auto")
     rows = np.unique(np.linspace(0, B - 1, min(B, 48)).astype(int))
     assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), f"c5 B={B}")
 
@@ -123,7 +125,7 @@ def test_parity_c5_sweep_sampled(B):
 def test_parity_c4_full_batch_sampled():
     """BASELINE.json's largest config at its full size (B = 1e5), the bench's launch configuration."""
     prob = make_problem("c4", device="cuda")
-    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "auto")
     # shard boundaries at 1/2/4/8 GPUs, plus every signal that did not run to S (checked against
     # the oracle too: an early stop must be the oracle's as well, or a flagged divergence)
     odd = np.flatnonzero((out["status"] != MAXITER) | (out["n_iter"] != prob.S))
@@ -188,7 +190,7 @@ def test_invalid_dictionary_and_args():
         assert r.X.shape == (0, 4)
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", LIB_MODES)
 def test_batch_invariance_bitwise(mode):
     """P8: signal b's result does not depend on B or on its position (no split-K in K1)."""
     prob = make_problem("c2", B=300)
@@ -196,6 +198,23 @@ def test_batch_invariance_bitwise(mode):
     part = run_gpu(prob.A, prob.Y[130:260], prob.S, None, mode)
     for key in ("support", "X", "resid", "n_iter", "status"):
         assert np.array_equal(full[key][130:260], part[key]), key
+
+
+@pytest.mark.parametrize("case", [("tiny", 16, {}), ("c2", 64, {}), ("c5", 20, {}), ("c5", 64, {"eps": 0.05}),
+                                  ("c3", 8, {}), ("c4", 2, {})], ids=lambda c: f"{c[0]}-B{c[1]}")
+def test_small_path_bitwise_equals_screened(case):
+    """The persistent small-batch kernel and the screened per-iteration path return the same bits:
+    n* is the exact FP32 argmax on both (rigorous screen window), and they share the append/residual
+    code (update_core.cuh).  Covers KC = 4 / 8 / 16 register tiles (M = 32 .. 2048) and eps stops."""
+    name, B, over = case
+    prob = make_problem(name, B=B, **over)
+    small = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "small")
+    scr = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+    assert small["launches"] == 2 and scr["launches"] == 1 + 2 * prob.S
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(small[key], scr[key]), key
+    rows = range(min(B, 8))
+    assert_no_bugs(parity(small, prob.A, prob.Y, prob.S, prob.eps, rows), f"small {name} B={B}")
 
 
 def _fields(r):
