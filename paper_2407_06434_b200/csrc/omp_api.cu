@@ -66,6 +66,10 @@ struct ompHandle_st {
   float* cstar = nullptr;
   float2* part = nullptr;   // screening epilogue: (B) x (Np / 128) x TOPK candidates
   int64_t capC = 0;         // rows of C (SIMT mode / ompCorrelate)
+  // split batches: the second half runs on side_stream so one half's L2-bound update overlaps the
+  // other half's tensor-core screen (OMP_B200_SPLIT=2)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // small-batch path (k_small.cu): partials (SMALL_MAX_B x SMs x SMALL_MAX_CTAS_PER_SM) + barrier
   int64_t small_limit = -1; // -1 automatic, 0 never, > 0 explicit maximum batch
   float4* pbest = nullptr;
@@ -217,7 +221,7 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
   const size_t planes = 2 * (size_t)nB * h->Mp;                  // two buffers
   bool ok = dalloc(h->R32, planes) && dalloc(h->F, (size_t)nB * ldf) && dalloc(h->U, (size_t)nB * nS) &&
             dalloc(h->nstar, (size_t)nB) && dalloc(h->cstar, (size_t)nB) && dalloc(h->rslot, 2 * (size_t)nB) &&
-            dalloc(h->slot, (size_t)nB) && dalloc(h->live, (size_t)nS + 2);
+            dalloc(h->slot, (size_t)nB) && dalloc(h->live, 2 * ((size_t)nS + 2));
   if (ok && bf) ok = dalloc(h->Rb, planes);
   if (ok && x3) ok = dalloc(h->R_hi, planes) && dalloc(h->R_lo, planes);
   if (ok && tc) ok = dalloc(h->part, (size_t)nB * (h->Np / SCREEN_GROUP) * TOPK);
@@ -263,6 +267,111 @@ static ompStatus_t ensure_small(ompHandle_t h) {
   return OMP_OK;
 }
 
+// A contiguous slice of the batch workspace: rows [r0, r0 + B) of every per-signal / per-slot buffer
+// (slots of a slice are numbered from 0 within it) and the slice's own live counters.
+struct WsView {
+  float* R32[2];
+  uint16_t* Rb[2];
+  float* Rhi[2];
+  float* Rlo[2];
+  float* rslot[2];
+  int32_t* slot;
+  int32_t* live;
+  int32_t* nstar;
+  float* cstar;
+  float2* part;
+  float* F;
+  float* U;
+};
+
+static WsView ws_view(const ompHandle_t h, int64_t r0, int idx) {
+  WsView w;
+  for (int buf = 0; buf < 2; ++buf) {
+    const size_t off = ((size_t)buf * h->capB + r0) * h->Mp;
+    w.R32[buf] = h->R32 + off;
+    w.Rb[buf] = h->Rb ? h->Rb + off : nullptr;
+    w.Rhi[buf] = h->R_hi ? h->R_hi + off : nullptr;
+    w.Rlo[buf] = h->R_lo ? h->R_lo + off : nullptr;
+    w.rslot[buf] = h->rslot + (size_t)buf * h->capB + r0;
+  }
+  w.slot = h->slot + r0;
+  w.live = h->live + (size_t)idx * (h->capS + 2);
+  w.nstar = h->nstar + r0;
+  w.cstar = h->cstar + r0;
+  w.part = h->part ? h->part + (size_t)r0 * (h->Np / SCREEN_GROUP) * TOPK : nullptr;
+  w.F = h->F + (size_t)r0 * h->ldf;
+  w.U = h->U + (size_t)r0 * h->ldu;
+  return w;
+}
+
+static Operand view_operand(const ompHandle_t h, const WsView& w, int64_t B, int buf) {
+  if (!tc_mode(h)) return Operand{{w.R32[buf], nullptr}, B, h->Mp};
+  if (tc_kind(h) == KIND_BF16) return Operand{{w.Rb[buf], nullptr}, B, h->Mp};
+  return Operand{{w.Rhi[buf], w.Rlo[buf]}, B, h->Mp};
+}
+
+// init + S screened iterations for one slice of the batch, on stream st
+static ompStatus_t enqueue_screened(ompHandle_t h, const WsView& w, const float* Y, int64_t B, int64_t ldy,
+                                    int32_t S, float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
+                                    float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st,
+                                    Launcher& L) {
+  cudaError_t e = cudaMemsetAsync(w.live, 0, sizeof(int32_t) * ((size_t)S + 2), st);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  L.begin(0);
+  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, w.R32[0], w.Rb[0], w.Rhi[0], w.Rlo[0],
+                        X, ldx, support, lds, resid, n_iter, status, w.slot, w.live, w.rslot[0], st);
+  L.end(0);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  const Operand At = atoms_operand(h);
+  for (int32_t k = 0; k < S; ++k) {
+    const int cur = k & 1, nxt = cur ^ 1;
+    const Operand R = view_operand(h, w, B, cur);
+    if (tc_mode(h)) {
+      // a2: tensor-core screen C~ = A^T R_k over the live rows; the epilogue keeps the in-window
+      // entries of every 128-atom group
+      L.begin(1);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, w.live + k, w.rslot[cur], h->window,
+                              w.part, st);
+      L.end(1);
+      if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    } else {
+      // a2: FP32 SIMT GEMM C = A^T R_k over the live rows; a3: n* = argmax |c_n| / ||a_n||
+      L.begin(1);
+      e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, w.live + k, st);
+      L.end(1);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      L.begin(2);
+      e = launch_select(h->C, h->Np, B, h->N, h->inv_norm, status, w.slot, w.nstar, w.cstar, st);
+      L.end(2);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    }
+    // a3 (tensor-core modes: exact re-evaluation of the screen's candidates) + a4 factor append +
+    // a5 residual / eps mask / next operand planes, one CTA per live signal
+    UpdateLaunch U;
+    U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
+    U.part = tc_mode(h) ? w.part : nullptr;
+    U.groups = (int)(h->Np / SCREEN_GROUP);
+    U.window = h->window;
+    U.nstar = w.nstar; U.cstar = w.cstar;
+    U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
+    U.Y = Y; U.ldy = ldy; U.F = w.F; U.ldf = h->ldf; U.U = w.U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
+    U.support = support; U.lds = lds;
+    U.R32in = w.R32[cur];
+    U.R32 = w.R32[nxt]; U.Rb = w.Rb[nxt]; U.Rhi = w.Rhi[nxt]; U.Rlo = w.Rlo[nxt];
+    U.rslot_out = w.rslot[nxt];
+    U.slot = w.slot; U.live_next = w.live + k + 1;
+    U.resid = resid; U.n_iter = n_iter; U.status = status;
+    U.l2_persist_bytes = h->l2_persist;
+    L.begin(3);
+    e = launch_update(U, st);
+    L.end(3);
+    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  }
+  return OMP_OK;
+}
+
 // The launch sequence of one batch (also what gets captured into the CUDA graph).
 static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int32_t S,
                                  float eps, float* X, int64_t ldx, int32_t* support, int64_t lds,
@@ -298,59 +407,38 @@ static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64
     h->lastS = S;
     return OMP_OK;
   }
-  cudaError_t e = cudaMemsetAsync(h->live, 0, sizeof(int32_t) * ((size_t)S + 2), st);
-  if (e != cudaSuccess) return cuda_fail(h, e);
-  L.begin(0);
-  e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, r32_buf(h, 0), rb_buf(h, 0), rhi_buf(h, 0), rlo_buf(h, 0),
-                        X, ldx, support, lds, resid, n_iter, status, h->slot, h->live, h->rslot, st);
-  L.end(0);
-  if (e != cudaSuccess) return cuda_fail(h, e);
-  const Operand At = atoms_operand(h);
-  for (int32_t k = 0; k < S; ++k) {
-    const int cur = k & 1, nxt = cur ^ 1;
-    const Operand R = resid_operand(h, B, cur);
-    if (tc_mode(h)) {
-      // a2: tensor-core screen C~ = A^T R_k over the live rows; the epilogue keeps the in-window
-      // entries of every 128-atom group
-      L.begin(1);
-      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, h->live + k, h->rslot + (size_t)cur * h->capB, h->window,
-                              h->part, st);
-      L.end(1);
-      if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
-      if (e != cudaSuccess) return cuda_fail(h, e);
-    } else {
-      // a2: FP32 SIMT GEMM C = A^T R_k over the live rows; a3: n* = argmax |c_n| / ||a_n||
-      L.begin(1);
-      e = launch_corr_simt(R, At, h->Mp, h->C, h->Np, h->Np, h->live + k, st);
-      L.end(1);
-      if (e != cudaSuccess) return cuda_fail(h, e);
-      L.begin(2);
-      e = launch_select(h->C, h->Np, B, h->N, h->inv_norm, status, h->slot, h->nstar, h->cstar, st);
-      L.end(2);
+  int parts = 1;
+  static int env_split = -1;
+  if (env_split < 0) {
+    const char* ev = getenv("OMP_B200_SPLIT");
+    env_split = ev ? atoi(ev) : 1;
+  }
+  if (env_split >= 2 && tc_mode(h) && B >= 2048) parts = 2;
+  if (parts == 1) {
+    s = enqueue_screened(h, ws_view(h, 0, 0), Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st, L);
+    if (s != OMP_OK) return s;
+  } else {
+    // fork: half 1 on the side stream, ordered after everything already on `st`; join at the end
+    if (!h->side_stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_fail(h, e);
     }
-    // a3 (tensor-core modes: exact re-evaluation of the screen's candidates) + a4 factor append +
-    // a5 residual / eps mask / next operand planes, one CTA per live signal
-    UpdateLaunch U;
-    U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
-    U.part = tc_mode(h) ? h->part : nullptr;
-    U.groups = (int)(h->Np / SCREEN_GROUP);
-    U.window = h->window;
-    U.nstar = h->nstar; U.cstar = h->cstar;
-    U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
-    U.Y = Y; U.ldy = ldy; U.F = h->F; U.ldf = h->ldf; U.U = h->U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
-    U.support = support; U.lds = lds;
-    U.R32in = r32_buf(h, cur);
-    U.R32 = r32_buf(h, nxt); U.Rb = rb_buf(h, nxt); U.Rhi = rhi_buf(h, nxt); U.Rlo = rlo_buf(h, nxt);
-    U.rslot_out = h->rslot + (size_t)nxt * h->capB;
-    U.slot = h->slot; U.live_next = h->live + k + 1;
-    U.resid = resid; U.n_iter = n_iter; U.status = status;
-    U.l2_persist_bytes = h->l2_persist;
-    L.begin(3);
-    e = launch_update(U, st);
-    L.end(3);
-    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+    const int64_t B0 = (B / 2 + 127) / 128 * 128, B1 = B - B0;
+    cudaError_t e = cudaEventRecord(h->fork_ev, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side_stream, h->fork_ev, 0);
     if (e != cudaSuccess) return cuda_fail(h, e);
+    Launcher L1{h, h->side_stream};
+    s = enqueue_screened(h, ws_view(h, 0, 0), Y, B0, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st, L);
+    if (s == OMP_OK)
+      s = enqueue_screened(h, ws_view(h, B0, 1), Y + B0 * ldy, B1, ldy, S, eps, X + B0 * ldx, ldx,
+                           support + B0 * lds, lds, resid + B0, n_iter + B0, status + B0, h->side_stream, L1);
+    if (s != OMP_OK) return s;
+    e = cudaEventRecord(h->join_ev, h->side_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, h->join_ev, 0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.count += L1.count;
   }
   h->last_launches = L.count;
   h->lastB = B;
