@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for single-GPU testing")
+    p.add_argument("--algo", default="auto", choices=["auto", "residual", "projection"],
+                   help="iteration formulation (ompSetAlgorithm); auto = the library's cost model")
     p.add_argument("--small-limit", type=int, default=-1,
                    help="small-batch persistent-kernel limit (-1 library default, 0 never)")
     p.add_argument("--no-kernel-profile", action="store_true",
@@ -143,12 +145,23 @@ def ncu_traffic(kernel_key: str, config_name: str):
 
 
 # ------------------------------------------------------------------------------ roofline model
-def kernel_work(cfg, B, mode):
+def kernel_work(cfg, B, mode, path="residual"):
     """Algorithmic work per launch (SURVEY §8(d) per signal-iteration, x the B signals one launch covers,
     at the mean support size k = (S-1)/2 of a full run).  DESIGN.md §6 states each figure."""
     M, N, S = cfg["M"], cfg["N"], cfg["S"]
     Mp = -(-M // 64) * 64
     k = (S - 1) / 2.0
+    if path == "projection":
+        Np = -(-N // 256) * 256
+        # update: argmax over the p row, append, p = P0 - sum_j x_j G[s_j, :] (k+1 Gram rows from L2)
+        hbm = B * (4.0 * Np * 3 + 4.0 * k * (k + 1) / 2 + 4.0 * (k + 2) * 3)   # p read + P0 read + p write, F
+        l2 = B * 4.0 * Np * (k + 1)
+        return {
+            # P0 = A^T Y once per batch: FP32 FFMA GEMM, 2 M N flops per signal
+            "correlation": ("alu", 2.0 * M * N * B, "TFLOP/s", None),
+            "update": ("l2", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
+            "init": ("hbm", B * 4.0 * (2 * M + Mp), "GB/s", None),
+        }
     tiles = math.ceil(N / 256)
     planes = {"bf16": 2.0, "3xtf32": 8.0, "simt": 0.0}[mode]
     # update = exact selection + factor append + residual, split into streamed (HBM) and gathered (L2)
@@ -213,6 +226,8 @@ def main():
     h = OMP(A, mode=args.mode)
     if args.small_limit != -1:
         h.set_small_batch_limit(args.small_limit)
+    if args.algo != "auto":
+        h.set_algorithm(args.algo)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -239,7 +254,11 @@ def main():
     clocks.start()
     step_ms = []
     launches = 0
+    # inputs smaller than 2x L2 (126 MB): flush L2 between timed steps by writing 256 MB
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if Y_np.nbytes < (252 << 20) else None
     for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
         barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -290,7 +309,8 @@ def main():
                "d2h_bytes_per_step": int(sum(o.nbytes for o in outs)) * world}
 
     # roofline of the dominant kernel (events measured live over the timed steps, this rank)
-    work = kernel_work(cfg, B, args.mode)
+    path = h.last_path()
+    work = kernel_work(cfg, B, args.mode, path)
     dom = max((k for k in kern if k in work), key=lambda k: kern[k][0])
     bound, per_launch, unit, split = work[dom]
     t_launch = kern[dom][0] / max(1, kern[dom][1]) / 1e3
@@ -305,6 +325,10 @@ def main():
             peak = base / 2.0 / (3.0 if args.mode == "3xtf32" else 1.0) if args.mode != "simt" else 74.0
             peak_src = "bf16 sustained x nominal tf32/bf16 ratio 1/2 (/3 for 3 products)" if args.mode != "simt" \
                 else "FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz"
+    elif bound == "alu":
+        # FP32 FFMA peak: 148 SMs x 128 lanes x 2 flops x 1.965 GHz (guide unit counts and max clock)
+        achieved = per_launch / t_launch / 1e12
+        peak, peak_src = 74.4, "FP32 FFMA: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md §6)"
     elif bound == "l2":
         # the update kernel's bytes all pass through L2 (the atom-row gather hits it; the streamed rows
         # come from HBM through it): its roof is the L2 read bandwidth measured on a B200 by
@@ -328,8 +352,9 @@ def main():
     for k, (tot_ms, n_l) in other.items():
         b2, w2, u2, _ = work[k]
         t2 = tot_ms / n_l / 1e3
-        if b2 == "tensor":
-            tp = (peaks or {}).get("bf16_tflops_sustained", 1400.0) if args.mode == "bf16" else None
+        if b2 in ("tensor", "alu"):
+            tp = 74.4 if b2 == "alu" else (
+                (peaks or {}).get("bf16_tflops_sustained", 1400.0) if args.mode == "bf16" else None)
             roofline["others"][k] = {"bound": b2, "achieved_tflops": w2 / t2 / 1e12, "launch_ms": t2 * 1e3,
                                      "frac": (w2 / t2 / 1e12 / tp) if tp else None}
         else:
@@ -354,7 +379,9 @@ def main():
                                    + (f" sigma={cfg['sigma']} eps={eps:.4g}" if eps else " noiseless"),
                        "M": M, "N": N, "S": S, "global_batch": B_total, "per_gpu_batch": per,
                        "mode": args.mode, "screen_dtype": {"bf16": "bf16", "3xtf32": "tf32x3", "simt": "none"}[args.mode],
-                       "l2": "inputs larger than L2 (Y %.0f MB/rank)" % (Y_np.nbytes / 1e6),
+                       "l2": ("L2 flushed between timed steps (256 MB write; Y %.1f MB/rank)" if flush is not None
+                              else "inputs larger than L2 (Y %.0f MB/rank)") % (Y_np.nbytes / 1e6),
+                       "path": path,
                        "parallelism": f"batch-shard x{world}"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "kernels": kernels,

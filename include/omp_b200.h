@@ -144,6 +144,20 @@ ompStatus_t ompGetFactor(ompHandle_t handle, int64_t b0, int64_t count, float* F
 ompStatus_t ompProfileEnable(ompHandle_t handle, int enable);
 ompStatus_t ompProfileRead(ompHandle_t handle, double* ms, int64_t* launches, int reset);
 
+/* ompSetAlgorithm — which formulation of the iteration a batch runs:
+ *   OMP_ALGO_RESIDUAL: the residual path (a2-a5 above; the small-batch kernel for small B);
+ *   OMP_ALGO_PROJECTION: the paper's algorithm v0 -- projections p = A^T r_k instead of the
+ *     M-length residual.  Once per batch P0 = A^T Y (FP32 GEMM); per iteration, one kernel
+ *     selects n* = argmax |p_n| / ||a_n||, appends the factor and recomputes
+ *     p = P0 - sum_j x_j G[s_j, :] (O(N k) per signal).  The eps test uses
+ *     ||r||^2 = ||y||^2 - ||u||^2 (q_j orthonormal); the returned resid_norm is the exact
+ *     ||y - A_S x|| computed after the last iteration.  Cheaper when M is large against N
+ *     (the paper's Yale shape, M = 8064, N = 1207).
+ *   OMP_ALGO_AUTO (default): a per-signal-iteration cost model picks one.
+ *   OMP_ERR_INVALID_ARG for any other value.                                               */
+typedef enum { OMP_ALGO_AUTO = 0, OMP_ALGO_RESIDUAL = 1, OMP_ALGO_PROJECTION = 2 } ompAlgorithm_t;
+ompStatus_t ompSetAlgorithm(ompHandle_t handle, int algorithm);
+
 /* ompSetSmallBatchLimit — batches of at most `max_batch` signals run on the small-batch path:
  *   one persistent cooperative kernel for all S iterations (exact FP32 correlation over all N
  *   atoms, then factor append + residual per signal, PAPER.md:243 on
@@ -153,6 +167,12 @@ ompStatus_t ompProfileRead(ompHandle_t handle, double* ms, int64_t* launches, in
  *   the path also needs Mp <= 2048 and B x Mp x 4 bytes of shared memory (<= 150 KB), else the
  *   screened path runs.  OMP_ERR_INVALID_ARG for max_batch < -1.                           */
 ompStatus_t ompSetSmallBatchLimit(ompHandle_t handle, int64_t max_batch);
+
+/* Which path the last ompBatch ran: OMP_PATH_RESIDUAL (screen + update per iteration),
+ * OMP_PATH_SMALL (the small-batch persistent kernel), OMP_PATH_PROJECTION (algorithm v0);
+ * -1 for a NULL handle.                                                                   */
+typedef enum { OMP_PATH_RESIDUAL = 0, OMP_PATH_SMALL = 1, OMP_PATH_PROJECTION = 2 } ompPath_t;
+int ompGetLastPath(ompHandle_t handle);
 
 /* Kernel launches issued by the last ompBatch (for launch accounting).                   */
 int64_t ompGetLaunchCount(ompHandle_t handle);

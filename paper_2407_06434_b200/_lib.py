@@ -32,6 +32,10 @@ OMP_SIG_NAN = 3
 OMP_CORR_BF16 = 0
 OMP_CORR_FP32_SIMT = 1
 OMP_CORR_3XTF32 = 2
+OMP_ALGO_AUTO = 0
+OMP_ALGO_RESIDUAL = 1
+OMP_ALGO_PROJECTION = 2
+PATH_NAMES = ("residual", "small", "projection")
 OMP_NUM_KERNEL_SLOTS = 5
 KERNEL_SLOTS = ("init", "correlation", "select", "update", "small")
 
@@ -51,6 +55,8 @@ SIGNATURES = {
     "ompProfileRead": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), c_int]),
     "ompGetLaunchCount": (c_int64, [c_void_p]),
     "ompSetSmallBatchLimit": (c_int, [c_void_p, c_int64]),
+    "ompSetAlgorithm": (c_int, [c_void_p, c_int]),
+    "ompGetLastPath": (c_int, [c_void_p]),
     "ompDestroy": (c_int, [c_void_p]),
     "ompGetErrorString": (c_char_p, [c_int]),
     "ompGetErrorDetail": (c_int64, [c_void_p]),

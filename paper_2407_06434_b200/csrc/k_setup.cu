@@ -112,7 +112,7 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
                              float* __restrict__ Rlo, float* __restrict__ X, int64_t ldx,
                              int32_t* __restrict__ support, int64_t lds, float* __restrict__ resid,
                              int32_t* __restrict__ n_iter, int32_t* __restrict__ status, int32_t* __restrict__ slot,
-                             int32_t* __restrict__ live0, float* __restrict__ rslot) {
+                             int32_t* __restrict__ live0, float* __restrict__ rslot, double* __restrict__ ynorm2) {
   __shared__ double red[32];
   __shared__ int s_slot;
   const int64_t b = blockIdx.x;
@@ -129,6 +129,7 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
   const double ss = block_sum_double((double)part, red);
   if (threadIdx.x == 0) {
     const float rn = (float)sqrt(ss);
+    if (ynorm2) ynorm2[b] = ss;
     n_iter[b] = 0;
     int st;
     if (!isfinite(ss)) {
@@ -160,10 +161,40 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
-                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st) {
+                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st, double* ynorm2) {
   if (B == 0) return cudaSuccess;
   k_batch_init<<<(unsigned)B, 128, 0, st>>>(Y, ldy, M, Mp, S, eps, R32, (__nv_bfloat16*)Rb, R_hi, R_lo, X, ldx,
-                                            support, lds, resid, n_iter, status, slot, live0, rslot);
+                                            support, lds, resid, n_iter, status, slot, live0, rslot, ynorm2);
+  return cudaGetLastError();
+}
+
+// Projection path, after the last iteration: the exact ||y_b - A_S x_b|| from gathered
+// atom rows, replacing the sqrt(||y||^2 - ||u||^2) the iterations used for the eps test (reading R22).
+__global__ void k_final_resid(const float* __restrict__ Y, int64_t ldy, int64_t M, const float* __restrict__ At,
+                              int64_t Mp, const float* __restrict__ X, int64_t ldx,
+                              const int32_t* __restrict__ support, int64_t lds, const int32_t* __restrict__ n_iter,
+                              const int32_t* __restrict__ status, float* __restrict__ resid) {
+  __shared__ double red[32];
+  const int64_t b = blockIdx.x;
+  const int k = n_iter[b];
+  if (k == 0 || status[b] == OMP_SIG_NAN) return;   // ||r|| = ||y|| (init) or NaN
+  const float* y = Y + b * ldy;
+  double part = 0.0;
+  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < k; ++j) acc = fmaf(X[b * ldx + j], At[(int64_t)support[b * lds + j] * Mp + m], acc);
+    const float r = y[m] - acc;
+    part += (double)r * r;
+  }
+  const double ss = block_sum_double(part, red);
+  if (threadIdx.x == 0) resid[b] = (float)sqrt(ss);
+}
+
+cudaError_t launch_final_resid(const float* Y, int64_t B, int64_t ldy, int64_t M, const float* At, int64_t Mp,
+                               const float* X, int64_t ldx, const int32_t* support, int64_t lds,
+                               const int32_t* n_iter, const int32_t* status, float* resid, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  k_final_resid<<<(unsigned)B, 256, 0, st>>>(Y, ldy, M, At, Mp, X, ldx, support, lds, n_iter, status, resid);
   return cudaGetLastError();
 }
 

@@ -357,7 +357,8 @@ cudaError_t launch_small(const UpdateLaunch& L, float4* pbest, unsigned int* bar
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
   a.support = L.support; a.lds = L.lds; a.R32in = L.R32; a.R32 = L.R32;
   a.Rb = nullptr; a.Rhi = nullptr; a.Rlo = nullptr; a.rslot_out = nullptr; a.slot = nullptr; a.live_next = nullptr;
-  a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status;
+  a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status; a.ynorm2 = nullptr;
+  a.At_res = nullptr; a.Mp_res = 0; a.M_res = 0; a.Y_res = nullptr; a.ldy_res = 0;
   s.B = L.B;
   s.pbest = pbest;
   s.bar = bar;

@@ -27,14 +27,19 @@ constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N
 
 // MINB: resident CTAs per SM the register budget must allow.  The kernel is latency-bound on its L2
 // gather and needs >= 8 CTAs of 128 threads per SM (measured: 2x slower at fewer, flat above).
-template <bool REFINE, int T, int CH, int MINB = 1024 / T>
+// SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
+// candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
+constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
+
+template <int SEL, int T, int CH, int MINB = 1024 / T>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
+  constexpr bool REFINE = (SEL == SEL_SCREEN);
   const int64_t b = blockIdx.x;
   if (a.status[b] != SIG_RUNNING) return;
   const int k = a.k;
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
-  const int cur_slot = a.slot[b];       // this signal's row in the current live set
+  const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update):
   //   [the fp32 residual row (refine): Mp floats] [w, z, u, xs: Sp floats each] [ss, ro: Sp ints each]
   //   [cand: RF_CAP ints (refine)]
@@ -151,6 +156,38 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
       sel_n = any_nan ? SEL_NAN : (ok ? r.n : SEL_DEGENERATE);
       sel_c = ok ? r.c : 0.f;
     }
+  } else if constexpr (SEL == SEL_PROJ) {
+    // exact argmax over the projections p_n = <r_k, a_n> (FP32): lowest index on ties
+    const float rn = a.resid[b];
+    const float* prow = a.R32in + (int64_t)cur_slot * a.Mp;
+    Cand best{-1.f, 0x7fffffff, 0.f};
+    bool nan_c = false;
+    for (int64_t n = tid; n < a.N; n += T) {
+      const float c = prow[n];
+      nan_c |= isnan(c);
+      const Cand cd{fabsf(c) * a.inv_norm[n], (int)n, c};
+      if (cand_better(cd, best)) best = cd;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Cand oth{__shfl_xor_sync(0xffffffffu, best.w, o), __shfl_xor_sync(0xffffffffu, best.n, o),
+                     __shfl_xor_sync(0xffffffffu, best.c, o)};
+      if (cand_better(oth, best)) best = oth;
+    }
+    if (lane == 0) red_c[warp] = best;
+    const int any_nan = __syncthreads_or(nan_c);
+    if (tid == 0) {
+      Cand r = red_c[0];
+#pragma unroll
+      for (int i = 1; i < T / 32; ++i)
+        if (cand_better(red_c[i], r)) r = red_c[i];
+      const bool ok = r.w > 0.f && r.n < a.N;
+      // (the u-based ||r|| is not used here: it can cancel to 0 while r is not; max |p| decides)
+      if (!isfinite(rn) || any_nan) sel_n = SEL_NAN;
+      else if (!ok) sel_n = SEL_DEGENERATE;
+      else sel_n = r.n;
+      sel_c = ok ? r.c : 0.f;
+    }
   } else {
     if (tid == 0) {
       sel_n = a.nstar[b];
@@ -165,12 +202,12 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     return;
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, &sel_n};
-  append_residual<T, CH>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, 2, 2, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
 }
 
-template <bool REFINE, int T, int CH, int MINB = 1024 / T>
+template <int SEL, int T, int CH, int MINB = 1024 / T>
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
-  auto kern = k_update<REFINE, T, CH, MINB>;
+  auto kern = k_update<SEL, T, CH, MINB>;
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   static bool opted = false;
   if (!opted) {
@@ -199,27 +236,27 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <bool REFINE>
+template <int SEL>
 static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   // float4 chunks per row -> (T, CH), T * CH == q4 at powers of two.  k_small.cu uses the same map:
   // the tail's reductions depend on T, and the two paths must agree bit for bit.
   const int64_t q4 = a.Mp / 4;
-  if (q4 <= 32) return launch_t<REFINE, 32, 1>(a, B, smem, persist, st);
-  if (q4 <= 64) return launch_t<REFINE, 64, 1>(a, B, smem, persist, st);
-  if (q4 <= 128) return launch_t<REFINE, 128, 1>(a, B, smem, persist, st);
-  if (q4 <= 256) return launch_t<REFINE, 128, 2>(a, B, smem, persist, st);
+  if (q4 <= 32) return launch_t<SEL, 32, 1>(a, B, smem, persist, st);
+  if (q4 <= 64) return launch_t<SEL, 64, 1>(a, B, smem, persist, st);
+  if (q4 <= 128) return launch_t<SEL, 128, 1>(a, B, smem, persist, st);
+  if (q4 <= 256) return launch_t<SEL, 128, 2>(a, B, smem, persist, st);
   if (q4 <= 512) {
     static int minb = -1;          // OMP_B200_UPDATE_MINB: register budget for 10 or 12 CTAs per SM
     if (minb < 0) {
       const char* env = getenv("OMP_B200_UPDATE_MINB");
       minb = env ? atoi(env) : 0;
     }
-    if (minb == 10) return launch_t<REFINE, 128, 4, 10>(a, B, smem, persist, st);
-    if (minb == 12) return launch_t<REFINE, 128, 4, 12>(a, B, smem, persist, st);
-    return launch_t<REFINE, 128, 4>(a, B, smem, persist, st);
+    if (minb == 10) return launch_t<SEL, 128, 4, 10>(a, B, smem, persist, st);
+    if (minb == 12) return launch_t<SEL, 128, 4, 12>(a, B, smem, persist, st);
+    return launch_t<SEL, 128, 4>(a, B, smem, persist, st);
   }
-  if (q4 <= 1024) return launch_t<REFINE, 256, 4>(a, B, smem, persist, st);
-  if (q4 <= 2048) return launch_t<REFINE, 256, 8>(a, B, smem, persist, st);
+  if (q4 <= 1024) return launch_t<SEL, 256, 4>(a, B, smem, persist, st);
+  if (q4 <= 2048) return launch_t<SEL, 256, 8>(a, B, smem, persist, st);
   return cudaErrorNotSupported;   // M > 8192
 }
 
@@ -232,12 +269,14 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
   a.support = L.support; a.lds = L.lds; a.R32in = L.R32in; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb;
   a.Rhi = L.Rhi; a.Rlo = L.Rlo; a.rslot_out = L.rslot_out; a.slot = L.slot; a.live_next = L.live_next;
-  a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status;
+  a.resid = L.resid; a.n_iter = L.n_iter; a.status = L.status; a.ynorm2 = L.ynorm2;
+  a.At_res = L.At_res; a.Mp_res = L.Mp_res; a.M_res = L.M_res; a.Y_res = L.Y_res; a.ldy_res = L.ldy_res;
   const bool refine = L.part != nullptr;
   const int64_t Sp = (L.k + 4) & ~3;
   const size_t smem = (refine ? (size_t)L.Mp * 4 : 0) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
-  return refine ? launch_r<true>(a, L.B, smem, L.l2_persist_bytes, st)
-                : launch_r<false>(a, L.B, smem, L.l2_persist_bytes, st);
+  if (refine) return launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);
+  if (L.ynorm2) return launch_r<SEL_PROJ>(a, L.B, smem, L.l2_persist_bytes, st);
+  return launch_r<SEL_GIVEN>(a, L.B, smem, L.l2_persist_bytes, st);
 }
 
 }  // namespace ompb

@@ -70,6 +70,11 @@ struct ompHandle_st {
   // other half's tensor-core screen (OMP_B200_SPLIT=2)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // projection path (algorithm v0): P0 = A^T Y, the projection rows p, ||y||^2
+  int algo = OMP_ALGO_AUTO;
+  int64_t capP = 0;
+  float *P0 = nullptr, *P = nullptr, *Pwork = nullptr;
+  double* yy = nullptr;
   // small-batch path (k_small.cu): partials (SMALL_MAX_B x SMs x SMALL_MAX_CTAS_PER_SM) + barrier
   int64_t small_limit = -1; // -1 automatic, 0 never, > 0 explicit maximum batch
   float4* pbest = nullptr;
@@ -85,6 +90,7 @@ struct ompHandle_st {
   // diagnostics
   int64_t err_detail = 0;
   int64_t last_launches = 0;
+  int last_path = OMP_PATH_RESIDUAL;
   bool profile = false;
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> ev_pool;
@@ -95,6 +101,7 @@ struct ompHandle_st {
     cudaGraphExec_t exec = nullptr;
     GraphKey key{};
     int64_t launches = 0;
+    int path = 0;
     uint64_t used = 0;
   };
   static constexpr int kGraphCache = 4;
@@ -248,7 +255,8 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
 // crossover on B200 (the persistent kernel wins below B ~ 6..12 on c2..c5): B <= 8
 // and its exact correlation (B N Mp FMAs per iteration, phase A of k_small.cu) within 2^26.
 static bool use_small(ompHandle_t h, int64_t B, int32_t S) {
-  if (!tc_mode(h) || h->small_limit == 0 || !small_path_supported(B, h->Mp, S)) return false;
+  if (!tc_mode(h) || h->small_limit == 0 || h->algo == OMP_ALGO_PROJECTION || !small_path_supported(B, h->Mp, S))
+    return false;
   if (h->small_limit > 0) return B <= h->small_limit;
   return B <= 8 && (double)B * (double)h->N * (double)h->Mp <= 67108864.0;
 }
@@ -261,9 +269,51 @@ static ompStatus_t ensure_small(ompHandle_t h) {
   if (!dalloc(h->pbest, (size_t)SMALL_MAX_B * sms * SMALL_MAX_CTAS_PER_SM) || !dalloc(h->gbar, 1)) {
     dfree(h->pbest);
     dfree(h->gbar);
+    dfree(h->P0);
+    dfree(h->P);
+    dfree(h->Pwork);
+    dfree(h->yy);
     cudaGetLastError();
     return OMP_ERR_NOMEM;
   }
+  return OMP_OK;
+}
+
+// Projection path (the paper's algorithm v0): selection from p = A^T r_k, which is
+// recomputed each iteration as P0 - sum_j x_j G[s_j, :] (O(N k) per signal, no M-length residual).
+// Automatic choice by a cost model per signal-iteration: the residual path pays the
+// screen (2 M N flops on the tensor cores) plus an M-wide gather of k + 2 atom rows; the projection
+// path pays an N-wide gather of k + 2 Gram rows plus, amortised over S, the FP32 GEMM P0 = A^T Y.
+static bool use_proj(ompHandle_t h, int64_t B, int32_t S) {
+  if (h->algo == OMP_ALGO_RESIDUAL || B == 0) return false;
+  if (h->algo == OMP_ALGO_PROJECTION) return true;
+  const double kk = S / 2.0 + 2.0, M = (double)h->M, N = (double)h->N;
+  const double t_res = 2.0 * M * N / 1.4e15 + kk * (double)h->Mp * 4.0 / 2.0e13;
+  const double t_proj = kk * (double)h->Np * 4.0 / 2.0e13 + (double)h->Np * 8.0 / 6.5e12 + 2.0 * M * N / (S * 6.0e13);
+  return t_proj < t_res;
+}
+
+constexpr int64_t kP0Chunk = 1024;   // K slab of the P0 GEMM (fixed: the result must not depend on B)
+
+static ompStatus_t ensure_proj(ompHandle_t h, int64_t B) {
+  if (B <= h->capP) return OMP_OK;
+  dfree(h->P0);
+  dfree(h->P);
+  dfree(h->Pwork);
+  dfree(h->yy);
+  h->capP = 0;
+  const size_t slabs = (size_t)corr_simt_splitk_slabs(h->Mp, kP0Chunk);
+  if (!dalloc(h->P0, (size_t)B * h->Np) || !dalloc(h->P, (size_t)B * h->Np) || !dalloc(h->yy, (size_t)B) ||
+      !dalloc(h->Pwork, slabs * B * h->Np)) {
+    dfree(h->P0);
+    dfree(h->P);
+    dfree(h->Pwork);
+    dfree(h->yy);
+    cudaGetLastError();
+    return OMP_ERR_NOMEM;
+  }
+  h->capP = B;
+  invalidate_graph(h);
   return OMP_OK;
 }
 
@@ -403,6 +453,53 @@ static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64
     if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
     if (e != cudaSuccess) return cuda_fail(h, e);
     h->last_launches = L.count;
+    h->last_path = OMP_PATH_SMALL;
+    h->lastB = B;
+    h->lastS = S;
+    return OMP_OK;
+  }
+  if (use_proj(h, B, S)) {
+    // projection path: P0 = A^T Y (FP32 SIMT GEMM on the padded fp32 rows of Y), init, one kernel per
+    // iteration, exact final residual norms
+    L.begin(0);
+    cudaError_t e = launch_make_planes(Y, B, ldy, h->M, h->Mp, r32_buf(h, 0), nullptr, nullptr, nullptr, st);
+    L.end(0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(1);
+    e = launch_corr_simt_splitk(Operand{{r32_buf(h, 0), nullptr}, B, h->Mp}, Operand{{h->At, nullptr}, h->Np, h->Mp},
+                                h->Mp, h->P0, h->Np, h->Np, kP0Chunk, h->Pwork, st);
+    L.end(1);
+    ++L.count;                          // the slab reduction
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    L.begin(0);
+    e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, nullptr, nullptr, nullptr, nullptr, X, ldx, support, lds,
+                          resid, n_iter, status, nullptr, nullptr, nullptr, st, h->yy);
+    L.end(0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    for (int32_t k = 0; k < S; ++k) {
+      UpdateLaunch U = {};
+      U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->N; U.Mp = h->Np;
+      U.groups = (int)(h->Np / SCREEN_GROUP);
+      U.At = h->G; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
+      U.Y = h->P0; U.ldy = h->Np; U.F = h->F; U.ldf = h->ldf; U.U = h->U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
+      U.support = support; U.lds = lds;
+      U.R32in = k == 0 ? h->P0 : h->P;
+      U.R32 = h->P;
+      U.resid = resid; U.n_iter = n_iter; U.status = status;
+      U.ynorm2 = h->yy;
+      U.At_res = h->At; U.Mp_res = h->Mp; U.M_res = h->M; U.Y_res = Y; U.ldy_res = ldy;
+      L.begin(3);
+      e = launch_update(U, st);
+      L.end(3);
+      if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    }
+    L.begin(0);
+    e = launch_final_resid(Y, B, ldy, h->M, h->At, h->Mp, X, ldx, support, lds, n_iter, status, resid, st);
+    L.end(0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    h->last_launches = L.count;
+    h->last_path = OMP_PATH_PROJECTION;
     h->lastB = B;
     h->lastS = S;
     return OMP_OK;
@@ -441,6 +538,7 @@ static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64
     L.count += L1.count;
   }
   h->last_launches = L.count;
+  h->last_path = OMP_PATH_RESIDUAL;
   h->lastB = B;
   h->lastS = S;
   return OMP_OK;
@@ -455,6 +553,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
                              float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   ompStatus_t s = ensure_workspace(h, B, S);   // allocations happen outside any capture
   if (s == OMP_OK && use_small(h, B, S)) s = ensure_small(h);
+  else if (s == OMP_OK && use_proj(h, B, S)) s = ensure_proj(h, B);
   if (s != OMP_OK) return s;
   static int env_graph = -1;
   if (env_graph < 0) {
@@ -493,11 +592,13 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     }
     hit->key = key;
     hit->launches = h->last_launches;
+    hit->path = h->last_path;
   }
   hit->used = ++h->graph_tick;
   cudaError_t e = cudaGraphLaunch(hit->exec, st);
   if (e != cudaSuccess) return cuda_fail(h, e);
   h->last_launches = hit->launches;
+  h->last_path = hit->path;
   h->lastB = B;
   h->lastS = S;
   return OMP_OK;
@@ -535,6 +636,15 @@ const char* ompGetErrorString(ompStatus_t s) {
 int64_t ompGetErrorDetail(ompHandle_t h) { return h ? h->err_detail : g_create_detail; }
 
 int64_t ompGetLaunchCount(ompHandle_t h) { return h ? h->last_launches : 0; }
+
+int ompGetLastPath(ompHandle_t h) { return h ? h->last_path : -1; }
+
+ompStatus_t ompSetAlgorithm(ompHandle_t h, int algorithm) {
+  if (!h || algorithm < OMP_ALGO_AUTO || algorithm > OMP_ALGO_PROJECTION) return OMP_ERR_INVALID_ARG;
+  if (h->algo != algorithm) invalidate_graph(h);
+  h->algo = algorithm;
+  return OMP_OK;
+}
 
 ompStatus_t ompSetSmallBatchLimit(ompHandle_t h, int64_t max_batch) {
   if (!h || max_batch < -1) return OMP_ERR_INVALID_ARG;

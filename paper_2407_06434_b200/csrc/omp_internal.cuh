@@ -45,6 +45,11 @@ struct Operand {
 // FP32 SIMT GEMM (round-to-nearest, sequential K): C written for rows < live rows, n < ncols
 cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                              int64_t ncols, const int32_t* live_rows, cudaStream_t st);
+// split-K form: K in slabs of kchunk, partials (slabs x rows x ldc floats of `work`) summed in slab
+// order by a second kernel; 2 launches
+int64_t corr_simt_splitk_slabs(int64_t K, int64_t kchunk);
+cudaError_t launch_corr_simt_splitk(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
+                                    int64_t ncols, int64_t kchunk, float* work, cudaStream_t st);
 // tcgen05 screening GEMM on normalised atoms; C~ stored times ||a_n|| (diagnostics / numerics tests)
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, const float* norm, cudaStream_t st);
@@ -73,7 +78,12 @@ cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
-                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st);
+                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st,
+                              double* ynorm2 = nullptr);
+// projection path: exact ||y - A_S x|| per signal after the last iteration
+cudaError_t launch_final_resid(const float* Y, int64_t B, int64_t ldy, int64_t M, const float* At, int64_t Mp,
+                               const float* X, int64_t ldx, const int32_t* support, int64_t lds,
+                               const int32_t* n_iter, const int32_t* status, float* resid, cudaStream_t st);
 
 // ---- a3 + a4 + a5 fused per signal (k_update.cu) ----
 struct UpdateLaunch {
@@ -111,6 +121,13 @@ struct UpdateLaunch {
   int32_t* n_iter;
   int32_t* status;
   size_t l2_persist_bytes;  // > 0: launch with a persisting L2 access-policy window over At
+  // projection path (algorithm v0): non-null selects it.  Then At := G, Y := P0 = A^T Y (ldy = Np),
+  // M := N, Mp := Np, R32in / R32 := the projection rows, part = nstar = nullptr
+  const double* ynorm2 = nullptr;
+  const float* At_res = nullptr;   // the fp32 atom rows, Mp_res apart, and y (ldy_res): exact ||r|| near eps
+  int64_t Mp_res = 0, M_res = 0;
+  const float* Y_res = nullptr;
+  int64_t ldy_res = 0;
 };
 cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st);
 // ---- small-batch path: all S iterations in one persistent cooperative kernel (k_small.cu) ----

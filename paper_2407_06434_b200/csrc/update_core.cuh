@@ -68,6 +68,12 @@ struct UpdateArgs {
   float* resid;
   int32_t* n_iter;
   int32_t* status;
+  const double* ynorm2; // projection path: ||y_b||^2 (the residual norm comes from u, reading R22)
+  // projection path: the dictionary itself, for the exact residual norm near the eps threshold
+  const float* At_res;
+  int64_t Mp_res, M_res;
+  const float* Y_res;
+  int64_t ldy_res;
 };
 
 struct Cand {
@@ -137,6 +143,20 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return r;
 }
 
+template <int T>
+__device__ __forceinline__ double block_sum_d(double v) {
+  __shared__ double redd[T / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) redd[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+#pragma unroll
+  for (int w = 0; w < T / 32; ++w) r += redd[w];
+  return r;
+}
+
 // one float4 chunk into a partial sum, in the fixed order w, z, y, x
 __device__ __forceinline__ float fma4(const float4 r, const float4 a, float s) {
   return fmaf(r.x, a.x, fmaf(r.y, a.y, fmaf(r.z, a.z, fmaf(r.w, a.w, s))));
@@ -202,6 +222,9 @@ struct TailSmem {
 };
 
 // a4 + a5 for signal b at iteration k with the selected atom n >= 0 and c* = <r_k, a_n>.
+// V0 (the projection path, paper's algorithm v0): the caller passes At := G,
+// Y := P0 = A^T Y, M := N, Mp := Np, so the "residual" this computes is the projection vector
+// p_{k+1} = A^T r_{k+1} = P0 - sum_j x_j G[s_j, :]; ||r_{k+1}|| = sqrt(||y||^2 - ||u||^2) (reading R22).
 // P: atom rows in flight per thread in the gather, ZC: columns per warp in z = F^T w (the
 // per-iteration kernel hides latency with 8 CTAs per SM and uses 2 / 2; the persistent small-batch
 // kernel has one CTA per signal on the critical path and uses more).  Neither changes the order of
@@ -213,7 +236,7 @@ struct TailSmem {
 // rows_sm (nullable): a shared-memory copy of the support's atom rows (row j at rows_sm + j q4,
 // j <= k; row k may still be landing by cp.async, waited for here) that the gather reads instead
 // of A^T in global memory -- the same values, so the same result.
-template <int T, int CH, int P = 2, int ZC = 2>
+template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false>
 __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
                                                 const float cst, const TailSmem& sm, const float* Fb,
                                                 float* Fs_append, const float4* rows_sm = nullptr) {
@@ -420,7 +443,32 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       part = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, fmaf(acc[c].w, acc[c].w, part))));
     }
   }
-  const float rr = block_sum<T>(part, sm.red);
+  float rr;
+  if constexpr (V0) {
+    // ||r_{k+1}||^2 = ||y||^2 - ||u_{k+1}||^2 (q_j orthonormal, u_j = q_j^T y, pin P9),
+    // in FP64.  The u_j carry FP32 errors, so where this estimate is within 1e-5 ||y||^2 of eps^2 the
+    // eps decision is taken on the exact ||y - A_S x|| instead (k+1 atom rows, reading R22).
+    double uu = 0.0;
+    for (int j = tid; j <= k; j += T) uu += (double)u[j] * (double)u[j];
+    uu = block_sum_d<T>(uu);
+    const double yy = a.ynorm2[b];
+    double r2 = fmax(yy - uu, 0.0);
+    const double e2 = (double)a.eps * (double)a.eps;
+    if (a.eps >= 0.f && fabs(r2 - e2) <= 1e-5 * yy) {
+      const float* yr = a.Y_res + b * a.ldy_res;
+      double pr = 0.0;
+      for (int64_t m = tid; m < a.M_res; m += T) {
+        float accm = 0.f;
+        for (int j = 0; j <= k; ++j) accm = fmaf(xs[j], a.At_res[(int64_t)ss[j] * a.Mp_res + m], accm);
+        const float r = yr[m] - accm;
+        pr += (double)r * (double)r;
+      }
+      r2 = block_sum_d<T>(pr);
+    }
+    rr = (float)r2;
+  } else {
+    rr = block_sum<T>(part, sm.red);
+  }
   OMP_TAIL_TRACE(5);
   if (tid == 0) {
     const float rn = sqrtf(rr);

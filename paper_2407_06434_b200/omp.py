@@ -165,9 +165,19 @@ class OMP:
         check(self.lib.ompProfileRead(self.handle, ms, n, int(reset)), "ompProfileRead", self.handle)
         return {name: (ms[i], n[i]) for i, name in enumerate(_lib.KERNEL_SLOTS)}
 
+    ALGOS = {"auto": 0, "residual": 1, "projection": 2}
+
+    def set_algorithm(self, algo: str):
+        """'auto' (default), 'residual' or 'projection' (the paper's algorithm v0), see ompSetAlgorithm."""
+        check(self.lib.ompSetAlgorithm(self.handle, self.ALGOS[algo]), "ompSetAlgorithm", self.handle)
+
     def set_small_batch_limit(self, max_batch: int):
         """-1 automatic (default), 0 never, else the largest batch run by the persistent kernel."""
         check(self.lib.ompSetSmallBatchLimit(self.handle, int(max_batch)), "ompSetSmallBatchLimit", self.handle)
+
+    def last_path(self) -> str:
+        """'residual', 'small' or 'projection': the path the last batch ran."""
+        return _lib.PATH_NAMES[int(self.lib.ompGetLastPath(self.handle))]
 
     def launch_count(self) -> int:
         return int(self.lib.ompGetLaunchCount(self.handle))

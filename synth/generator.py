@@ -41,6 +41,9 @@ CONFIGS = {
     "c4": dict(M=2048, N=8192, S=128, B=100000, sparsity=128, sigma=0.0, eps=None, seed=4),
     # c5: batch-size sweep B = 1 .. 1e6 (nested prefixes of one stream)
     "c5": dict(M=512, N=2048, S=50, B=1000000, sparsity=50, sigma=0.0, eps=None, seed=5),
+    # the paper's Yale shape: A in R^{8064 x 1207}, 1207 signals, S = 30 -- tall (M > N),
+    # where the projection path (algorithm v0) is the cheaper formulation; synthetic 30-sparse signals
+    "yale": dict(M=8064, N=1207, S=30, B=1207, sparsity=30, sigma=0.0, eps=None, seed=6),
 }
 C5_SWEEP = (1, 10, 100, 1000, 10000, 100000, 1000000)
 

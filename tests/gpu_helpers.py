@@ -17,8 +17,10 @@ def eps32(eps):
 # test "modes": the library's correlation modes on the screened (per-iteration) path, plus "small":
 # the small-batch persistent kernel (bf16 handle, small-batch limit 64; larger batches fall back to
 # the screened path)
-PATHS = {"bf16": ("bf16", 0), "3xtf32": ("3xtf32", 0), "simt": ("simt", 0), "small": ("bf16", 64),
-         "auto": ("bf16", -1)}   # "auto": the library default (what bench.py and users run)
+PATHS = {"bf16": ("bf16", 0, "residual"), "3xtf32": ("3xtf32", 0, "residual"), "simt": ("simt", 0, "residual"),
+         "small": ("bf16", 64, "residual"),
+         "proj": ("bf16", 0, "projection"),     # the paper's algorithm v0 (projection path)
+         "auto": ("bf16", -1, "auto")}          # the library default (what bench.py and users run)
 
 
 def run_gpu(A_np, Y_np, S, eps=None, mode="bf16", handle=None):
@@ -27,16 +29,17 @@ def run_gpu(A_np, Y_np, S, eps=None, mode="bf16", handle=None):
     A = torch.from_numpy(A_np).cuda()
     Y = torch.from_numpy(np.ascontiguousarray(Y_np)).cuda()
     own = handle is None
-    lib_mode, small = PATHS[mode]
+    lib_mode, small, algo = PATHS[mode]
     h = OMP(A, mode=lib_mode) if own else handle
     try:
         if own:
             h.set_small_batch_limit(small)
+            h.set_algorithm(algo)
         res = h.batch(Y, S, eps32(eps))
         torch.cuda.synchronize()
         out = dict(support=res.support.cpu().numpy(), X=res.X.cpu().numpy(),
                    resid=res.resid_norm.cpu().numpy(), n_iter=res.n_iter.cpu().numpy(),
-                   status=res.status.cpu().numpy(), launches=h.launch_count())
+                   status=res.status.cpu().numpy(), launches=h.launch_count(), path=h.last_path())
     finally:
         if own:
             h.close()

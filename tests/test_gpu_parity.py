@@ -16,7 +16,8 @@ from oracle import DEGENERATE, EPS, MAXITER, NAN
 from synth import make_dictionary, make_problem, make_signals
 
 pytestmark = pytest.mark.gpu
-MODES = ["bf16", "3xtf32", "simt", "small"]    # gpu_helpers.PATHS; "small" = persistent kernel
+MODES = ["bf16", "3xtf32", "simt", "small", "proj"]   # gpu_helpers.PATHS ("small" = persistent kernel,
+                                                     # "proj" = projection path / algorithm v0)
 LIB_MODES = ["bf16", "3xtf32", "simt"]
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
@@ -90,8 +91,11 @@ def test_parity_tiny(mode):
     rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, range(prob.B))
     d = assert_no_bugs(rep, f"tiny/{mode}")
     assert d["counts"].get("exact", 0) == prob.B
-    # init + per-iteration kernels, or init + the persistent kernel
-    assert out["launches"] == (2 if mode == "small" else 1 + (3 if mode == "simt" else 2) * prob.S)
+    # init + per-iteration kernels; init + the persistent kernel; Y planes + P0 GEMM + init + one kernel
+    # per iteration + final residual
+    want = {"small": 2, "proj": prob.S + 5, "simt": 1 + 3 * prob.S}.get(mode, 1 + 2 * prob.S)
+    assert out["launches"] == want
+    assert out["path"] == {"small": "small", "proj": "projection"}.get(mode, "residual")
 
 
 @pytest.mark.parametrize("mode", LIB_MODES)
@@ -159,8 +163,14 @@ def test_edge_cases(mode):
     out = run_gpu(A, Y, 8, 0.0, mode)
     assert out["status"][1] == EPS and out["n_iter"][1] == 0 and np.all(out["support"][1] == -1)
     assert out["status"][2] == NAN and out["n_iter"][2] == 0
-    assert out["status"][3] in (DEGENERATE, MAXITER)
+    # an exact 2-atom fit: the residual path's FP32 r is tiny but nonzero, so it goes on and stops
+    # DEGENERATE (or at S); the projection path's ||r||^2 = ||y||^2 - ||u||^2 may cancel to exactly
+    # 0 <= eps = 0 and stop by eps after the two atoms (reading R22)
+    ok = (DEGENERATE, MAXITER, EPS) if mode == "proj" else (DEGENERATE, MAXITER)
+    assert out["status"][3] in ok
     assert set(out["support"][3][:2]) == {3, 50}
+    if out["status"][3] == EPS:
+        assert out["n_iter"][3] == 2
     out = run_gpu(A, Y[4:5], 8, float(yn) * 1.0001, mode)
     assert out["status"][0] == EPS and out["n_iter"][0] == 0
     assert out["resid"][0] == pytest.approx(yn, rel=1e-6)
@@ -210,11 +220,36 @@ def test_small_path_bitwise_equals_screened(case):
     prob = make_problem(name, B=B, **over)
     small = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "small")
     scr = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+    assert small["path"] == "small" and scr["path"] == "residual"
     assert small["launches"] == 2 and scr["launches"] == 1 + 2 * prob.S
     for key in ("support", "X", "resid", "n_iter", "status"):
         assert np.array_equal(small[key], scr[key]), key
     rows = range(min(B, 8))
     assert_no_bugs(parity(small, prob.A, prob.Y, prob.S, prob.eps, rows), f"small {name} B={B}")
+
+
+@pytest.mark.parametrize("case", [("c2", 300, {}), ("c3", 400, {}), ("c5", 200, {}), ("yale", 96, {})],
+                         ids=lambda c: f"{c[0]}-B{c[1]}")
+def test_projection_path_parity(case):
+    """The projection path (algorithm v0) against the oracle: selections from
+    p = P0 - sum_j x_j G[s_j, :], the eps test from ||y||^2 - ||u||^2 (reading R22), exact final ||r||."""
+    name, B, over = case
+    prob = make_problem(name, B=B, **over)
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "proj")
+    assert out["launches"] == prob.S + 5 and out["path"] == "projection"
+    rows = range(B) if prob.A.shape[0] <= 1024 else range(0, B, 6)
+    d = assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), f"proj {name} B={B}")
+    assert d["counts"].get("exact", 0) + d["counts"].get("flagged_ok", 0) >= 0.97 * len(rows)
+
+
+def test_auto_algorithm_picks_projection_for_tall_dictionaries():
+    """Cost model: the Yale shape (M = 8064 > N = 1207) runs the projection path, c2 the residual path."""
+    yale = make_problem("yale", B=16)
+    assert run_gpu(yale.A, yale.Y, yale.S, None, "auto")["path"] == "projection"
+    c2 = make_problem("c2", B=8)
+    assert run_gpu(c2.A, c2.Y, c2.S, None, "auto")["path"] == "small"          # B <= 8
+    c2b = make_problem("c2", B=100)
+    assert run_gpu(c2b.A, c2b.Y, c2b.S, None, "auto")["path"] == "residual"
 
 
 def _fields(r):
