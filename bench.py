@@ -33,6 +33,9 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "OMP signals/sec"
+# the paper's own GPU numbers for the exact workload shapes it published (BASELINE.md §1a, App. B
+# Table 2 rows 9-10: best of its naive / v0 GPU times, B = 100, other hardware): vs_baseline
+PAPER_SIGNALS_PER_S = {"t2m1024": 100 / 0.546, "t2m2048": 100 / 4.392}
 UNIT = "signals/s"
 
 
@@ -374,7 +377,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": (value / PAPER_SIGNALS_PER_S[args.config]) if args.config in PAPER_SIGNALS_PER_S else None,
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: M={M} N={N} S={S} B={B_total}"
                                    + (f" sigma={cfg['sigma']} eps={eps:.4g}" if eps else " noiseless"),
                        "M": M, "N": N, "S": S, "global_batch": B_total, "per_gpu_batch": per,

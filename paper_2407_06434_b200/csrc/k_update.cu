@@ -31,7 +31,9 @@ constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
 constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
 
-template <int SEL, int T, int CH, int MINB = 1024 / T>
+// P: atom rows in flight per thread in the gather (2 at 8 CTAs per SM; more when the batch leaves
+// the SMs nearly empty and one CTA's memory parallelism is all a signal gets)
+template <int SEL, int T, int CH, int MINB = 1024 / T, int P = 2>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool REFINE = (SEL == SEL_SCREEN);
   const int64_t b = blockIdx.x;
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   asm volatile("cp.async.commit_group;" ::: "memory");
   {
     const char* fp = reinterpret_cast<const char*>(a.F + b * a.ldf);
-    const uint32_t fbytes = (uint32_t)(((int64_t)k * (k + 1) / 2) * 4);
+    // (only while F_k fits L1 comfortably; a large one is read from L2 with loads in flight instead)
+    const uint32_t fbytes = (uint32_t)min((int64_t)k * (k + 1) / 2 * 4, (int64_t)64 * 1024);
     for (uint32_t o = (uint32_t)tid * 128u; o < fbytes; o += (uint32_t)T * 128u)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
     const char* yp = reinterpret_cast<const char*>(a.Y + b * a.ldy);
@@ -85,10 +88,10 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
     const float rn = a.resid[b];
-    const float2* P = a.part + (int64_t)cur_slot * a.groups * TOPK;
+    const float2* Pt = a.part + (int64_t)cur_slot * a.groups * TOPK;
     const int E = a.groups * TOPK;
     float vmax = -1.f;
-    for (int e = tid; e < E; e += T) vmax = fmaxf(vmax, P[e].x);
+    for (int e = tid; e < E; e += T) vmax = fmaxf(vmax, Pt[e].x);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     if (lane == 0) red[warp] = vmax;
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     const float thr = vmax - a.window * rn;
     bool full = false;
     for (int t = tid; t < a.groups; t += T) {
-      const float2 last = P[t * TOPK + TOPK - 1];
+      const float2 last = Pt[t * TOPK + TOPK - 1];
       const int nl = __float_as_int(last.y);
       if (nl == SEL_OVERFLOW && last.x >= thr) {         // more in-window entries than kept: all of it
         const int n0 = t * SCREEN_GROUP;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
         }
       } else {
         for (int j = 0; j < TOPK; ++j) {
-          const float2 p = P[t * TOPK + j];
+          const float2 p = Pt[t * TOPK + j];
           const int n = __float_as_int(p.y);
           if (p.x >= thr && n >= 0 && n < a.N) {
             const int at = atomicAdd(&ncand, 1);
@@ -202,12 +205,12 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     return;
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, &sel_n};
-  append_residual<T, CH, 2, 2, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, 2, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
 }
 
-template <int SEL, int T, int CH, int MINB = 1024 / T>
+template <int SEL, int T, int CH, int MINB = 1024 / T, int P = 2>
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
-  auto kern = k_update<SEL, T, CH, MINB>;
+  auto kern = k_update<SEL, T, CH, MINB, P>;
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   static bool opted = false;
   if (!opted) {
@@ -236,27 +239,32 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// (T, CH) for the row width; "few" = at most 2 CTAs per SM in the whole launch
+template <int SEL, int T, int CH>
+static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, bool few, cudaStream_t st) {
+  if (few) return launch_t<SEL, T, CH, 1, (16 / CH > 2 ? 16 / CH : 2)>(a, B, smem, persist, st);
+  return launch_t<SEL, T, CH>(a, B, smem, persist, st);
+}
+
 template <int SEL>
 static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   // float4 chunks per row -> (T, CH), T * CH == q4 at powers of two.  k_small.cu uses the same map:
-  // the tail's reductions depend on T, and the two paths must agree bit for bit.
-  const int64_t q4 = a.Mp / 4;
-  if (q4 <= 32) return launch_t<SEL, 32, 1>(a, B, smem, persist, st);
-  if (q4 <= 64) return launch_t<SEL, 64, 1>(a, B, smem, persist, st);
-  if (q4 <= 128) return launch_t<SEL, 128, 1>(a, B, smem, persist, st);
-  if (q4 <= 256) return launch_t<SEL, 128, 2>(a, B, smem, persist, st);
-  if (q4 <= 512) {
-    static int minb = -1;          // OMP_B200_UPDATE_MINB: register budget for 10 or 12 CTAs per SM
-    if (minb < 0) {
-      const char* env = getenv("OMP_B200_UPDATE_MINB");
-      minb = env ? atoi(env) : 0;
-    }
-    if (minb == 10) return launch_t<SEL, 128, 4, 10>(a, B, smem, persist, st);
-    if (minb == 12) return launch_t<SEL, 128, 4, 12>(a, B, smem, persist, st);
-    return launch_t<SEL, 128, 4>(a, B, smem, persist, st);
+  // the tail's reductions depend on T, and the two paths must agree bit for bit (P does not matter).
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
   }
-  if (q4 <= 1024) return launch_t<SEL, 256, 4>(a, B, smem, persist, st);
-  if (q4 <= 2048) return launch_t<SEL, 256, 8>(a, B, smem, persist, st);
+  const bool few = B <= 2 * (int64_t)sms;
+  const int64_t q4 = a.Mp / 4;
+  if (q4 <= 32) return launch_tc<SEL, 32, 1>(a, B, smem, persist, few, st);
+  if (q4 <= 64) return launch_tc<SEL, 64, 1>(a, B, smem, persist, few, st);
+  if (q4 <= 128) return launch_tc<SEL, 128, 1>(a, B, smem, persist, few, st);
+  if (q4 <= 256) return launch_tc<SEL, 128, 2>(a, B, smem, persist, few, st);
+  if (q4 <= 512) return launch_tc<SEL, 128, 4>(a, B, smem, persist, few, st);
+  if (q4 <= 1024) return launch_tc<SEL, 256, 4>(a, B, smem, persist, few, st);
+  if (q4 <= 2048) return launch_tc<SEL, 256, 8>(a, B, smem, persist, few, st);
   return cudaErrorNotSupported;   // M > 8192
 }
 

@@ -277,7 +277,24 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       acc_z[c] = 0.f;
     }
     const int jl = min(j0 + ZC, k) - 1;   // last column of the group
-    for (int i = lane; i <= jl; i += 32) {
+    int i = lane;
+    // long columns (F_k of a large S lives in L2): four rows' loads in flight, FMAs in the same order
+    for (; i + 96 <= jl; i += 128) {
+      float cv[4][ZC], wv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ii = i + 32 * q;
+        wv[q] = w[ii];
+#pragma unroll
+        for (int c = 0; c < ZC; ++c) cv[q][c] = (ii <= j0 + c && j0 + c < k) ? col[c][ii] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < ZC; ++c)
+          if (i + 32 * q <= j0 + c && j0 + c < k) acc_z[c] = fmaf(cv[q][c], wv[q], acc_z[c]);
+    }
+    for (; i <= jl; i += 32) {
       const float wi = w[i];
 #pragma unroll
       for (int c = 0; c < ZC; ++c)
@@ -313,6 +330,26 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
     int j = i & ~31;
     int o = j * (j + 1) / 2 + i;                  // offset of F[i, j] in the packed columns
+    // 8 column loads in flight (F_k of a large S lives in L2, not L1), the FMAs in the same order
+    for (; j + 8 <= k; j += 8) {
+      float f[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        f[q] = (j + q >= i) ? Fb[o] : 0.f;
+        o += j + q + 1;
+      }
+#pragma unroll
+      for (int g = 0; g < 8; g += 4) {
+        v0 = fmaf(f[g], z[j + g], v0);
+        t0 = fmaf(f[g], u[j + g], t0);
+        v1 = fmaf(f[g + 1], z[j + g + 1], v1);
+        t1 = fmaf(f[g + 1], u[j + g + 1], t1);
+        v2 = fmaf(f[g + 2], z[j + g + 2], v2);
+        t2 = fmaf(f[g + 2], u[j + g + 2], t2);
+        v3 = fmaf(f[g + 3], z[j + g + 3], v3);
+        t3 = fmaf(f[g + 3], u[j + g + 3], t3);
+      }
+    }
     for (; j + 4 <= k; j += 4) {
       const int o1 = o + j + 1, o2 = o1 + j + 2, o3 = o2 + j + 3;
       const float f0 = (j >= i) ? Fb[o] : 0.f;

@@ -44,6 +44,10 @@ CONFIGS = {
     # the paper's Yale shape: A in R^{8064 x 1207}, 1207 signals, S = 30 -- tall (M > N),
     # where the projection path (algorithm v0) is the cheaper formulation; synthetic 30-sparse signals
     "yale": dict(M=8064, N=1207, S=30, B=1207, sparsity=30, sigma=0.0, eps=None, seed=6),
+    # the paper's synthetic sweep (App. B Table 2 rows 9-10): N = 8M atoms, S = M/4, B = 100
+    # (reading R13: M measurements); S-sparse noiseless signals
+    "t2m1024": dict(M=1024, N=8192, S=256, B=100, sparsity=256, sigma=0.0, eps=None, seed=7),
+    "t2m2048": dict(M=2048, N=16384, S=512, B=100, sparsity=512, sigma=0.0, eps=None, seed=8),
 }
 C5_SWEEP = (1, 10, 100, 1000, 10000, 100000, 1000000)
 

@@ -242,6 +242,16 @@ def test_projection_path_parity(case):
     assert d["counts"].get("exact", 0) + d["counts"].get("flagged_ok", 0) >= 0.97 * len(rows)
 
 
+@pytest.mark.parametrize("name", ["t2m1024", "t2m2048"])
+def test_paper_sweep_shapes_sampled(name):
+    """The paper's own synthetic sweep shapes (App. B Table 2 rows 9-10: N = 8M, S = M/4, B = 100),
+    full batch in the bench's launch configuration, sampled rows against the oracle."""
+    prob = make_problem(name)
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "auto")
+    rows = [0, 37, 99] if name == "t2m1024" else [0, 99]
+    assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), name)
+
+
 def test_auto_algorithm_picks_projection_for_tall_dictionaries():
     """Cost model: the Yale shape (M = 8064 > N = 1207) runs the projection path, c2 the residual path."""
     yale = make_problem("yale", B=16)

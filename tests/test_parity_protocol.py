@@ -56,7 +56,7 @@ def test_generator_contract():
     assert np.array_equal(Y1[2:], Y2)              # per-signal streams: shard invariant
     Yn, truth = make_signals(A, [0, 1], 9, (3, 6), sigma=0.1, with_truth=True)
     assert all(3 <= len(s) <= 6 for s in truth.supports)
-    assert set(CONFIGS) == {"tiny", "c2", "c3", "c4", "c5", "yale"}
+    assert set(CONFIGS) == {"tiny", "c2", "c3", "c4", "c5", "yale", "t2m1024", "t2m2048"}
     p = make_problem("c3", B=3)
     assert p.eps is not None and abs(p.eps - 0.32) < 1e-12 and p.Y.shape == (3, 1024)
 
