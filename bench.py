@@ -350,6 +350,10 @@ def main():
                 "work_per_launch": per_launch, "launch_ms": t_launch * 1e3}
     if bound == "l2":
         roofline.update(roofline_extra)
+    # the measured peaks were taken at ~1.96 GHz; a long bench step runs power-capped (clocks.sm_mhz):
+    # the same fraction against the peak scaled to the clock the step actually ran at (context)
+    if bound in ("l2", "alu") and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        roofline["frac_at_bench_clock"] = roofline["frac"] * clk["sm_max_mhz"] / clk["sm_mhz"]
     other = {k: kern[k] for k in kern if k in work and k != dom and kern[k][1] > 0}
     roofline["others"] = {}
     for k, (tot_ms, n_l) in other.items():

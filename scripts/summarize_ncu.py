@@ -13,7 +13,8 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = {"k1_corr_tc": "correlation", "k1_corr_simt": "correlation", "k2_refine": "select", "k2_select": "select",
-        "k3_factor": "factor_append", "k4_residual": "residual", "k_batch_init": "init", "k_update": "update"}
+        "k3_factor": "factor_append", "k4_residual": "residual", "k_batch_init": "init", "k_update": "update",
+        "k_small": "small", "k_sum_slabs": "slab_sum", "k_final_resid": "final_resid", "k_make_planes": "planes"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -93,7 +94,7 @@ def main():
              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, v in sorted(share.items(), key=lambda kv: -kv[1]["total_ms"]):
         lines.append(f"| {k} | {v['launches']} | {v['total_ms']:.2f} | {100 * v['share']:.1f}% |")
-    lines += ["", "Full capture (`ncu --set full`, iteration 64 of the bench step):", "",
+    lines += ["", "Full capture (`ncu --set full`; which launches: see `scripts/profile_round.sh` / the round notes):", "",
               "| kernel | time ms | DRAM read GB | DRAM write GB | L2 bytes GB | DRAM % | L2 % | SM % | tensor % | regs |",
               "|---|---|---|---|---|---|---|---|---|---|"]
     for k, e in full.items():
