@@ -25,15 +25,19 @@ namespace ompb {
 
 constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N atoms)
 
-// MINB: resident CTAs per SM the register budget must allow.  The kernel is latency-bound on its L2
-// gather and needs >= 8 CTAs of 128 threads per SM (measured: 2x slower at fewer, flat above).
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
 constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
 
 // P: atom rows in flight per thread in the gather (2 at 8 CTAs per SM; more when the batch leaves
 // the SMs nearly empty and one CTA's memory parallelism is all a signal gets)
-template <int SEL, int T, int CH, int MINB = 1024 / T, int P = 2>
+// Resident threads per SM the register budget must allow: 1280 = 10 CTAs of 128 threads (51
+// registers).  The kernel is latency-bound on its L2 gather; measured at c4 (A/B builds on one box):
+// 6 CTAs 5.09 ms, 7: 4.82, 8: 4.66, 10: 4.52, 12: 4.53 ms per launch, despite the spills it costs.
+#ifndef OMP_UPDATE_CTAS
+#define OMP_UPDATE_CTAS 1280
+#endif
+template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool REFINE = (SEL == SEL_SCREEN);
   const int64_t b = blockIdx.x;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   append_residual<T, CH, P, 2, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
 }
 
-template <int SEL, int T, int CH, int MINB = 1024 / T, int P = 2>
+template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   auto kern = k_update<SEL, T, CH, MINB, P>;
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
