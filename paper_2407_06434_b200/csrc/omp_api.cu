@@ -66,10 +66,6 @@ struct ompHandle_st {
   float* cstar = nullptr;
   float2* part = nullptr;   // screening epilogue: (B) x (Np / 128) x TOPK candidates
   int64_t capC = 0;         // rows of C (SIMT mode / ompCorrelate)
-  // split batches: the second half runs on side_stream so one half's L2-bound update overlaps the
-  // other half's tensor-core screen (OMP_B200_SPLIT=2)
-  cudaStream_t side_stream = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // projection path (algorithm v0): P0 = A^T Y, the projection rows p, ||y||^2
   int algo = OMP_ALGO_AUTO;
   int64_t capP = 0;
@@ -504,39 +500,8 @@ static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64
     h->lastS = S;
     return OMP_OK;
   }
-  int parts = 1;
-  static int env_split = -1;
-  if (env_split < 0) {
-    const char* ev = getenv("OMP_B200_SPLIT");
-    env_split = ev ? atoi(ev) : 1;
-  }
-  if (env_split >= 2 && tc_mode(h) && B >= 2048) parts = 2;
-  if (parts == 1) {
-    s = enqueue_screened(h, ws_view(h, 0, 0), Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st, L);
-    if (s != OMP_OK) return s;
-  } else {
-    // fork: half 1 on the side stream, ordered after everything already on `st`; join at the end
-    if (!h->side_stream) {
-      cudaError_t e = cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming);
-      if (e != cudaSuccess) return cuda_fail(h, e);
-    }
-    const int64_t B0 = (B / 2 + 127) / 128 * 128, B1 = B - B0;
-    cudaError_t e = cudaEventRecord(h->fork_ev, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side_stream, h->fork_ev, 0);
-    if (e != cudaSuccess) return cuda_fail(h, e);
-    Launcher L1{h, h->side_stream};
-    s = enqueue_screened(h, ws_view(h, 0, 0), Y, B0, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st, L);
-    if (s == OMP_OK)
-      s = enqueue_screened(h, ws_view(h, B0, 1), Y + B0 * ldy, B1, ldy, S, eps, X + B0 * ldx, ldx,
-                           support + B0 * lds, lds, resid + B0, n_iter + B0, status + B0, h->side_stream, L1);
-    if (s != OMP_OK) return s;
-    e = cudaEventRecord(h->join_ev, h->side_stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, h->join_ev, 0);
-    if (e != cudaSuccess) return cuda_fail(h, e);
-    L.count += L1.count;
-  }
+  s = enqueue_screened(h, ws_view(h, 0, 0), Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st, L);
+  if (s != OMP_OK) return s;
   h->last_launches = L.count;
   h->last_path = OMP_PATH_RESIDUAL;
   h->lastB = B;
