@@ -226,7 +226,12 @@ def main():
     Y = torch.from_numpy(Y_np).to(dev)
     eps32 = None if eps is None else float(np.float32(eps))
 
+    # ompCreate (validation, norms, screen planes, Gram G = A^T A) timed on its own
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     h = OMP(A, mode=args.mode)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t_setup) * 1e3
     if args.small_limit != -1:
         h.set_small_batch_limit(args.small_limit)
     if args.algo != "auto":
@@ -393,6 +398,7 @@ def main():
                        "parallelism": f"batch-shard x{world}"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "kernels": kernels,
+            "setup_ms": setup_ms,
         }
         if parity_rep is not None:
             line["parity"] = parity_rep

@@ -313,6 +313,22 @@ def test_host_path_matches_device_path():
         assert np.array_equal(Xd[b], want)
 
 
+def test_host_path_chunked_pipeline_matches_device_path():
+    """ompBatchHost splits a large batch into chunks whose copies overlap the solve; the results are
+    bitwise those of one device call."""
+    import torch
+    from paper_2407_06434_b200 import OMP
+    prob = make_problem("c5", B=140000, device="cuda")     # >= 2 x 65536: two chunks
+    with OMP(torch.from_numpy(prob.A).cuda()) as h:
+        dev = h.batch(torch.from_numpy(prob.Y).cuda(), prob.S)
+        torch.cuda.synchronize()
+        host = h.batch_host(prob.Y, prob.S)
+        for key, a, b in (("support", dev.support, host.support), ("X", dev.X, host.X),
+                          ("resid", dev.resid_norm, host.resid_norm), ("n_iter", dev.n_iter, host.n_iter),
+                          ("status", dev.status, host.status)):
+            assert np.array_equal(a.cpu().numpy(), b), key
+
+
 def test_inverse_cholesky_state_identity():
     """P9 on the GPU's own factor: F_k V_k^T = I with V_k from numpy.linalg.cholesky."""
     import torch
