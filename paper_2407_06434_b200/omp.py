@@ -54,8 +54,8 @@ class OMP:
         self.device = A.device
         self.mode = mode
         At = A.t()
-        if not At.is_contiguous():
-            At = At.contiguous()      # column-major (atom-contiguous) layout the ABI takes
+        if At.stride(1) != 1:
+            At = At.contiguous()      # column-major (atom-contiguous) layout the ABI takes; lda = At.stride(0)
         h = ctypes.c_void_p()
         st = _stream_ptr(stream, self.device)
         rc = self.lib.ompCreate(ctypes.byref(h), self.device.index, At.data_ptr(), self.M, self.N,

@@ -313,6 +313,42 @@ def test_host_path_matches_device_path():
         assert np.array_equal(Xd[b], want)
 
 
+@pytest.mark.parametrize("mode", ["bf16", "simt", "small", "proj"])
+def test_strided_buffers_match_contiguous(mode):
+    """Leading dimensions beyond the minimum (lda > M, ldy > M, ldx / lds > S) on every path give the
+    same bits as contiguous buffers; nothing outside the logical rows/columns is touched."""
+    import torch
+    from gpu_helpers import PATHS
+    from paper_2407_06434_b200 import OMP, OMPResult
+    lib_mode, small, algo = PATHS[mode]
+    M, N, B, S = 100, 300, 6 if mode == "small" else 40, 9
+    A = make_dictionary(M, N, 21)
+    Y = make_signals(A, range(B), 21, 6, sigma=0.01)
+    Aw = torch.zeros((N, M + 5), dtype=torch.float32, device="cuda")   # atom n at row n: lda = M + 5
+    Aw[:, :M] = torch.from_numpy(A.T.copy()).cuda()
+    Yw = torch.full((B, M + 7), 7.0, dtype=torch.float32, device="cuda")
+    Yw[:, :M] = torch.from_numpy(Y).cuda()
+
+    def run(Adev, Ydev, out=None):
+        with OMP(Adev, mode=lib_mode) as h:
+            h.set_small_batch_limit(small)
+            h.set_algorithm(algo)
+            r = h.batch(Ydev, S, 0.05, out=out)
+            torch.cuda.synchronize()
+            assert h.last_path() == {"small": "small", "proj": "projection"}.get(mode, "residual")
+            return r
+
+    ref = run(torch.from_numpy(A).cuda(), torch.from_numpy(Y).cuda())
+    Xw = torch.full((B, S + 3), -9.0, dtype=torch.float32, device="cuda")
+    Sw = torch.full((B, S + 3), -9, dtype=torch.int32, device="cuda")
+    out = OMPResult(Xw[:, :S], Sw[:, :S], torch.empty(B, device="cuda"),
+                    torch.empty(B, dtype=torch.int32, device="cuda"), torch.empty(B, dtype=torch.int32, device="cuda"))
+    got = run(Aw[:, :M].t(), Yw[:, :M], out=out)
+    for key in ("X", "support", "resid_norm", "n_iter", "status"):
+        assert torch.equal(getattr(ref, key), getattr(got, key)), key
+    assert torch.all(Xw[:, S:] == -9.0) and torch.all(Sw[:, S:] == -9)
+
+
 def test_host_path_chunked_pipeline_matches_device_path():
     """ompBatchHost splits a large batch into chunks whose copies overlap the solve; the results are
     bitwise those of one device call."""
