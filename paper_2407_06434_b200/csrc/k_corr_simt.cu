@@ -151,7 +151,13 @@ cudaError_t launch_corr_simt_splitk(const Operand& R, const Operand& At, int64_t
                                      At.rows, K, work, ldc, ncols, nullptr, kchunk, zstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_sum_slabs<<<1184, 256, 0, st>>>(work, nz, zstride, R.rows, ncols, ldc, C, ldc);
+  return launch_sum_slabs(work, nz, zstride, R.rows, ncols, ldc, C, ldc, st);
+}
+
+cudaError_t launch_sum_slabs(const float* work, int64_t nz, int64_t zstride, int64_t rows, int64_t cols, int64_t ld,
+                             float* C, int64_t ldc, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  k_sum_slabs<<<1184, 256, 0, st>>>(work, nz, zstride, rows, cols, ld, C, ldc);
   return cudaGetLastError();
 }
 

@@ -206,6 +206,8 @@ struct EpiArgs {
   const int32_t* live_rows; // rows < *live_rows are live (live-set compaction); null: all rows
   const float* rslot;       // MODE_TOPK: ||r|| of the residual in each row
   float window;             // MODE_TOPK: screening window / ||r||
+  int kslab;                // MODE_STORE split-K: K blocks per slab (0: one slab); slab z -> C + z zstride
+  int64_t zstride;
 };
 
 struct Maps {
@@ -237,7 +239,11 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
   const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
-  const int num_tiles = tiles_m * tiles_n;
+  // split-K (MODE_STORE): the work items are (slab z, tile); slab z covers K blocks [z kslab, ...)
+  const int kslab = ep.kslab > 0 ? ep.kslab : num_kb;
+  const int nz = (num_kb + kslab - 1) / kslab;
+  const int tiles_mn = tiles_m * tiles_n;
+  const int num_tiles = tiles_mn * nz;
   const TileSched sched{tiles_m, tiles_n};
 
   if (threadIdx.x == 0) {
@@ -272,11 +278,13 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
       uint32_t phase = 0;
       const uint64_t keep = l2_policy(true), normal = l2_policy(false);
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        const int z = t / tiles_mn;
         int tm, tn;
-        sched.coords(t, tm, tn);
+        sched.coords(t - z * tiles_mn, tm, tn);
         const int row0 = tm * BM * CG + (int)rank * BM;
         const int atom0 = tn * BN + (int)rank * C_::BN_CTA;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = z * kslab, kb1 = min(num_kb, kb0 + kslab);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * C_::STAGE_BYTES;
           if (leader) mbar_expect_tx(&full[stage], C_::STAGE_BYTES * CG);
@@ -302,7 +310,9 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
         mbar_wait(&tempty[a], aphase ^ 1);
         fence_after();
         const uint32_t d = tmem_base + (uint32_t)(a * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int z = t / tiles_mn;
+        const int kb0 = z * kslab, kb1 = min(num_kb, kb0 + kslab);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint32_t base = smem_u32(smem + stage * C_::STAGE_BYTES);
@@ -312,11 +322,11 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
           for (int kk = 0; kk < K_::BK / K_::UK; ++kk) {
             const uint64_t off = (uint64_t)((kk * K_::UK * K_::ELEM) >> 4);   // +32 B per K step
             if constexpr (KIND == KIND_BF16) {
-              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb | kk) != 0);
+              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb != kb0 || kk != 0));
             } else {
               const uint64_t dr1 = desc_sw128(base + C_::R_BYTES);
               const uint64_t da1 = desc_sw128(base + 2 * C_::R_BYTES + C_::A_BYTES);
-              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb | kk) != 0);   // Rhi Ahi
+              mma<KIND, CG>(d, dr0 + off, da0 + off, C_::IDESC, (kb != kb0 || kk != 0));   // Rhi Ahi
               mma<KIND, CG>(d, dr1 + off, da0 + off, C_::IDESC, 1u);                // Rlo Ahi
               mma<KIND, CG>(d, dr0 + off, da1 + off, C_::IDESC, 1u);                // Rhi Alo
             }
@@ -335,8 +345,9 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     constexpr int HB = BN / 2;
     int it = 0;
     for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+      const int z = t / tiles_mn;
       int tm, tn;
-      sched.coords(t, tm, tn);
+      sched.coords(t - z * tiles_mn, tm, tn);
       const int a = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[a], aphase);
@@ -352,10 +363,16 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
           tmem_ld32(taddr + (uint32_t)(c * 32), v);
           const int64_t col0 = colh + c * 32;
           if (live) {
-            float* dst = ep.C + (int64_t)row * ep.ldc + col0;
+            float* dst = ep.C + (int64_t)z * ep.zstride + (int64_t)row * ep.ldc + col0;
+            if (ep.norm) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)      // undo the normalisation: C = A^T R
-              if (col0 + q < ep.ncols) dst[q] = v[q] * __ldg(ep.norm + col0 + q);
+              for (int q = 0; q < 32; ++q)    // undo the normalisation: C = A^T R
+                if (col0 + q < ep.ncols) dst[q] = v[q] * __ldg(ep.norm + col0 + q);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)    // raw operands (split-K partials)
+                if (col0 + q < ep.ncols) dst[q] = v[q];
+            }
           }
         }
       } else {
@@ -484,7 +501,9 @@ static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const 
   if (e != cudaSuccess) return e;
   const int tiles_m = (int)((R.rows + BM * CG - 1) / (BM * CG));
   const int tiles_n = (int)(At.rows / BN);
-  const int tiles = tiles_m * tiles_n;
+  const int nkb = (int)(K / K_::BK);
+  const int nz = ep.kslab > 0 ? (nkb + ep.kslab - 1) / ep.kslab : 1;
+  const int tiles = tiles_m * tiles_n * nz;
   const int max_clusters = num_sms() / CG;
   const int clusters = tiles < max_clusters ? tiles : max_clusters;
   cudaLaunchConfig_t cfg = {};
@@ -521,13 +540,24 @@ static cudaError_t dispatch(int kind, const Operand& R, const Operand& At, int64
 
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, const float* norm, cudaStream_t st) {
-  tc::EpiArgs ep{C, ldc, ncols, norm, nullptr, nullptr, nullptr, 0.f};   // all rows, no compaction
+  tc::EpiArgs ep{C, ldc, ncols, norm, nullptr, nullptr, nullptr, 0.f, 0, 0};   // all rows, no compaction
   return tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
+}
+
+cudaError_t launch_corr_tc_splitk(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
+                                  int64_t ncols, int64_t kslab, float* work, cudaStream_t st) {
+  const int64_t bk = kind == KIND_BF16 ? tc::Kind<KIND_BF16>::BK : tc::Kind<KIND_3XTF32>::BK;
+  if (kslab % bk != 0 || R.rows == 0) return R.rows == 0 ? cudaSuccess : cudaErrorInvalidValue;
+  const int64_t nz = (K + kslab - 1) / kslab;
+  tc::EpiArgs ep{work, ldc, ncols, nullptr, nullptr, nullptr, nullptr, 0.f, (int)(kslab / bk), R.rows * ldc};
+  cudaError_t e = tc::dispatch<tc::MODE_STORE>(kind, R, At, K, ep, st);
+  if (e != cudaSuccess) return e;
+  return launch_sum_slabs(work, nz, R.rows * ldc, R.rows, ncols, ldc, C, ldc, st);
 }
 
 cudaError_t launch_corr_tc_topk(int kind, const Operand& R, const Operand& At, int64_t K, const int32_t* live_rows,
                                 const float* rslot, float window, float2* part, cudaStream_t st) {
-  tc::EpiArgs ep{nullptr, 0, At.rows, nullptr, part, live_rows, rslot, window};
+  tc::EpiArgs ep{nullptr, 0, At.rows, nullptr, part, live_rows, rslot, window, 0, 0};
   return tc::dispatch<tc::MODE_TOPK>(kind, R, At, K, ep, st);
 }
 

@@ -70,6 +70,8 @@ struct ompHandle_st {
   int algo = OMP_ALGO_AUTO;
   int64_t capP = 0;
   float *P0 = nullptr, *P = nullptr, *Pwork = nullptr;
+  float *PAhi = nullptr, *PAlo = nullptr;   // 3xTF32 planes of the raw A^T (Np x Mp), built once
+  float *PYhi = nullptr, *PYlo = nullptr;   // 3xTF32 planes of Y (capP x Mp)
   double* yy = nullptr;
   // small-batch path (k_small.cu): partials (SMALL_MAX_B x SMs x SMALL_MAX_CTAS_PER_SM) + barrier
   int64_t small_limit = -1; // -1 automatic, 0 never, > 0 explicit maximum batch
@@ -272,6 +274,10 @@ static ompStatus_t ensure_small(ompHandle_t h) {
     dfree(h->P);
     dfree(h->Pwork);
     dfree(h->yy);
+    dfree(h->PAhi);
+    dfree(h->PAlo);
+    dfree(h->PYhi);
+    dfree(h->PYlo);
     cudaGetLastError();
     return OMP_ERR_NOMEM;
   }
@@ -292,22 +298,53 @@ static bool use_proj(ompHandle_t h, int64_t B, int32_t S) {
   return t_proj < t_res;
 }
 
-constexpr int64_t kP0Chunk = 1024;   // K slab of the P0 GEMM (fixed: the result must not depend on B)
+constexpr int64_t kP0Chunk = 1024;   // K slab of the SIMT P0 GEMM (fixed: the result must not depend on B)
+constexpr int64_t kP0SlabTC = 512;   // K slab of the tensor-core (3xTF32) P0 GEMM
 
-static ompStatus_t ensure_proj(ompHandle_t h, int64_t B) {
+// P0 = A^T Y on the tensor cores in 3xTF32 (default) or on the FP32 SIMT pipe (OMP_B200_P0=simt).
+// 3xTF32 in 512-deep slabs summed in FP32: the accumulator's truncation (§5) acts on 64 MMA
+// steps per slab only, and the operand split keeps ~2^-21 per product -- the same order as the FP32
+// SIMT GEMM's rounding over K = 8064 (the projection parity tests hold either way).
+static bool p0_on_tensor_cores() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OMP_B200_P0");
+    v = (e && e[0] == 's') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static ompStatus_t ensure_proj(ompHandle_t h, int64_t B, cudaStream_t st) {
+  if (!h->PAhi && p0_on_tensor_cores()) {
+    if (!dalloc(h->PAhi, (size_t)h->Np * h->Mp) || !dalloc(h->PAlo, (size_t)h->Np * h->Mp)) {
+      dfree(h->PAhi);
+      dfree(h->PAlo);
+      cudaGetLastError();
+      return OMP_ERR_NOMEM;
+    }
+    cudaError_t e = launch_make_planes(h->At, h->Np, h->Mp, h->Mp, h->Mp, nullptr, nullptr, h->PAhi, h->PAlo, st);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  }
   if (B <= h->capP) return OMP_OK;
   dfree(h->P0);
   dfree(h->P);
   dfree(h->Pwork);
   dfree(h->yy);
+  dfree(h->PYhi);
+  dfree(h->PYlo);
   h->capP = 0;
-  const size_t slabs = (size_t)corr_simt_splitk_slabs(h->Mp, kP0Chunk);
-  if (!dalloc(h->P0, (size_t)B * h->Np) || !dalloc(h->P, (size_t)B * h->Np) || !dalloc(h->yy, (size_t)B) ||
-      !dalloc(h->Pwork, slabs * B * h->Np)) {
+  const size_t s1 = (size_t)corr_simt_splitk_slabs(h->Mp, kP0Chunk), s2 = (size_t)((h->Mp + kP0SlabTC - 1) / kP0SlabTC);
+  const size_t slabs = s1 > s2 ? s1 : s2;
+  bool ok = dalloc(h->P0, (size_t)B * h->Np) && dalloc(h->P, (size_t)B * h->Np) && dalloc(h->yy, (size_t)B) &&
+            dalloc(h->Pwork, slabs * B * h->Np);
+  if (ok && p0_on_tensor_cores()) ok = dalloc(h->PYhi, (size_t)B * h->Mp) && dalloc(h->PYlo, (size_t)B * h->Mp);
+  if (!ok) {
     dfree(h->P0);
     dfree(h->P);
     dfree(h->Pwork);
     dfree(h->yy);
+    dfree(h->PYhi);
+    dfree(h->PYlo);
     cudaGetLastError();
     return OMP_ERR_NOMEM;
   }
@@ -460,15 +497,23 @@ static ompStatus_t enqueue_batch(ompHandle_t h, const float* Y, int64_t B, int64
   if (use_proj(h, B, S)) {
     // projection path: P0 = A^T Y (FP32 SIMT GEMM on the padded fp32 rows of Y), init, one kernel per
     // iteration, exact final residual norms
+    const bool tcp0 = p0_on_tensor_cores();
     L.begin(0);
-    cudaError_t e = launch_make_planes(Y, B, ldy, h->M, h->Mp, r32_buf(h, 0), nullptr, nullptr, nullptr, st);
+    cudaError_t e = tcp0 ? launch_make_planes(Y, B, ldy, h->M, h->Mp, nullptr, nullptr, h->PYhi, h->PYlo, st)
+                         : launch_make_planes(Y, B, ldy, h->M, h->Mp, r32_buf(h, 0), nullptr, nullptr, nullptr, st);
     L.end(0);
     if (e != cudaSuccess) return cuda_fail(h, e);
     L.begin(1);
-    e = launch_corr_simt_splitk(Operand{{r32_buf(h, 0), nullptr}, B, h->Mp}, Operand{{h->At, nullptr}, h->Np, h->Mp},
-                                h->Mp, h->P0, h->Np, h->Np, kP0Chunk, h->Pwork, st);
+    if (tcp0)
+      e = launch_corr_tc_splitk(KIND_3XTF32, Operand{{h->PYhi, h->PYlo}, B, h->Mp},
+                                Operand{{h->PAhi, h->PAlo}, h->Np, h->Mp}, h->Mp, h->P0, h->Np, h->Np, kP0SlabTC,
+                                h->Pwork, st);
+    else
+      e = launch_corr_simt_splitk(Operand{{r32_buf(h, 0), nullptr}, B, h->Mp}, Operand{{h->At, nullptr}, h->Np, h->Mp},
+                                  h->Mp, h->P0, h->Np, h->Np, kP0Chunk, h->Pwork, st);
     L.end(1);
     ++L.count;                          // the slab reduction
+    if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
     if (e != cudaSuccess) return cuda_fail(h, e);
     L.begin(0);
     e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, nullptr, nullptr, nullptr, nullptr, X, ldx, support, lds,
@@ -521,7 +566,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
                              float* resid, int32_t* n_iter, int32_t* status, cudaStream_t st) {
   ompStatus_t s = ensure_workspace(h, B, S);   // allocations happen outside any capture
   if (s == OMP_OK && use_small(h, B, S)) s = ensure_small(h);
-  else if (s == OMP_OK && use_proj(h, B, S)) s = ensure_proj(h, B);
+  else if (s == OMP_OK && use_proj(h, B, S)) s = ensure_proj(h, B, st);
   if (s != OMP_OK) return s;
   static int env_graph = -1;
   if (env_graph < 0) {

@@ -50,6 +50,13 @@ cudaError_t launch_corr_simt(const Operand& R, const Operand& At, int64_t K, flo
 int64_t corr_simt_splitk_slabs(int64_t K, int64_t kchunk);
 cudaError_t launch_corr_simt_splitk(const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                                     int64_t ncols, int64_t kchunk, float* work, cudaStream_t st);
+// C = sum of nz slab partials (slab z at work + z zstride), in slab order
+cudaError_t launch_sum_slabs(const float* work, int64_t nz, int64_t zstride, int64_t rows, int64_t cols, int64_t ld,
+                             float* C, int64_t ldc, cudaStream_t st);
+// tcgen05 GEMM C = R A^T on RAW operand planes, split-K in slabs of kslab (a multiple of the kind's
+// K block), partials summed in slab order (2 launches); 3xTF32 for an FP32-grade result
+cudaError_t launch_corr_tc_splitk(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
+                                  int64_t ncols, int64_t kslab, float* work, cudaStream_t st);
 // tcgen05 screening GEMM on normalised atoms; C~ stored times ||a_n|| (diagnostics / numerics tests)
 cudaError_t launch_corr_tc(int kind, const Operand& R, const Operand& At, int64_t K, float* C, int64_t ldc,
                            int64_t ncols, const float* norm, cudaStream_t st);
