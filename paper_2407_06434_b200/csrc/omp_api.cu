@@ -284,23 +284,6 @@ static ompStatus_t ensure_small(ompHandle_t h) {
   return OMP_OK;
 }
 
-// Projection path (the paper's algorithm v0, PAPER.md:178-182): selection from p = A^T r_k, which is
-// recomputed each iteration as P0 - sum_j x_j G[s_j, :] (O(N k) per signal, no M-length residual).
-// Automatic choice by a cost model per signal-iteration (DESIGN.md §6): the residual path pays the
-// screen (2 M N flops on the tensor cores) plus an M-wide gather of k + 2 atom rows; the projection
-// path pays an N-wide gather of k + 2 Gram rows plus, amortised over S, the FP32 GEMM P0 = A^T Y.
-static bool use_proj(ompHandle_t h, int64_t B, int32_t S) {
-  if (h->algo == OMP_ALGO_RESIDUAL || B == 0) return false;
-  if (h->algo == OMP_ALGO_PROJECTION) return true;
-  const double kk = S / 2.0 + 2.0, M = (double)h->M, N = (double)h->N;
-  const double t_res = 2.0 * M * N / 1.4e15 + kk * (double)h->Mp * 4.0 / 2.0e13;
-  const double t_proj = kk * (double)h->Np * 4.0 / 2.0e13 + (double)h->Np * 8.0 / 6.5e12 + 2.0 * M * N / (S * 6.0e13);
-  return t_proj < t_res;
-}
-
-constexpr int64_t kP0Chunk = 1024;   // K slab of the SIMT P0 GEMM (fixed: the result must not depend on B)
-constexpr int64_t kP0SlabTC = 512;   // K slab of the tensor-core (3xTF32) P0 GEMM
-
 // P0 = A^T Y on the tensor cores in 3xTF32 (default) or on the FP32 SIMT pipe (OMP_B200_P0=simt).
 // 3xTF32 in 512-deep slabs summed in FP32: the accumulator's truncation (§5) acts on 64 MMA
 // steps per slab only, and the operand split keeps ~2^-21 per product -- the same order as the FP32
@@ -313,6 +296,26 @@ static bool p0_on_tensor_cores() {
   }
   return v == 1;
 }
+
+// Projection path (the paper's algorithm v0, PAPER.md:178-182): selection from p = A^T r_k, which is
+// recomputed each iteration as P0 - sum_j x_j G[s_j, :] (O(N k) per signal, no M-length residual).
+// Automatic choice by a cost model per signal-iteration (DESIGN.md §6): the residual path pays the
+// screen (2 M N flops on the tensor cores) plus an M-wide gather of k + 2 atom rows; the projection
+// path pays an N-wide gather of k + 2 Gram rows plus, amortised over S, the FP32 GEMM P0 = A^T Y.
+static bool use_proj(ompHandle_t h, int64_t B, int32_t S) {
+  if (h->algo == OMP_ALGO_RESIDUAL || B == 0) return false;
+  if (h->algo == OMP_ALGO_PROJECTION) return true;
+  const double kk = S / 2.0 + 2.0, M = (double)h->M, N = (double)h->N;
+  const double t_res = 2.0 * M * N / 1.4e15 + kk * (double)h->Mp * 4.0 / 2.0e13;
+  // P0 = A^T Y: ~1e14 flop/s measured on the tensor cores (3xTF32 split-K incl. planes and slab sum),
+  // ~4e13 on the SIMT pipe
+  const double p0_rate = p0_on_tensor_cores() ? 1.0e14 : 4.0e13;
+  const double t_proj = kk * (double)h->Np * 4.0 / 2.0e13 + (double)h->Np * 8.0 / 6.5e12 + 2.0 * M * N / (S * p0_rate);
+  return t_proj < t_res;
+}
+
+constexpr int64_t kP0Chunk = 1024;   // K slab of the SIMT P0 GEMM (fixed: the result must not depend on B)
+constexpr int64_t kP0SlabTC = 512;   // K slab of the tensor-core (3xTF32) P0 GEMM
 
 static ompStatus_t ensure_proj(ompHandle_t h, int64_t B, cudaStream_t st) {
   if (!h->PAhi && p0_on_tensor_cores()) {
