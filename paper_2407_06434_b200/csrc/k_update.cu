@@ -19,11 +19,32 @@
 #include <math.h>
 #include <stdlib.h>
 
+#ifdef OMP_UPDATE_TRACE
+// diagnostic build only (-DOMP_UPDATE_TRACE, scripts/trace_update.py): per-phase clock64 deltas of
+// thread 0, summed over every CTA of the launch at iteration g_upd_trace_k
+__device__ int g_upd_trace_k = -1;
+__device__ unsigned long long g_upd_clk[16];
+#define UPD_TRACE(p)                                                                   \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && a.k == g_upd_trace_k) {                                    \
+      const unsigned long long t_ = clock64();                                         \
+      atomicAdd(&g_upd_clk[(p)], t_ - upd_t0_);                                        \
+      upd_t0_ = t_;                                                                    \
+    }                                                                                  \
+  } while (0)
+#define OMP_TAIL_TRACE(p) UPD_TRACE(4 + (p))
+#else
+#define UPD_TRACE(p)
+#endif
 #include "update_core.cuh"
 
 namespace ompb {
 
 constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N atoms)
+#ifndef OMP_UPDATE_ZC
+#define OMP_UPDATE_ZC 2
+#endif
+constexpr int ZC_UPD = OMP_UPDATE_ZC;   // columns per warp in z = F^T w (interleaving only)
 
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
@@ -42,6 +63,9 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool REFINE = (SEL == SEL_SCREEN);
   const int64_t b = blockIdx.x;
   if (a.status[b] != SIG_RUNNING) return;
+#ifdef OMP_UPDATE_TRACE
+  unsigned long long upd_t0_ = clock64();
+#endif
   const int k = a.k;
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
@@ -140,8 +164,10 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
         }
       }
     }
+    UPD_TRACE(0);
     asm volatile("cp.async.wait_all;" ::: "memory");   // residual row (and ss, u) landed
     full = __syncthreads_or(full);
+    UPD_TRACE(1);
     Cand best{-1.f, 0x7fffffff, 0.f};
     bool nan_c = false;
     const int count = full ? (int)a.N : min(ncand, RF_CAP);
@@ -203,13 +229,20 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   asm volatile("cp.async.wait_all;" ::: "memory");     // ss, u (SIMT path: first wait)
   __syncthreads();
+  UPD_TRACE(2);
   const int n = sel_n;
   if (n < 0) {
     if (tid == 0) a.status[b] = (n == SEL_NAN) ? OMP_SIG_NAN : OMP_SIG_DEGENERATE;
     return;
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, &sel_n};
-  append_residual<T, CH, P, 2, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
+#ifdef OMP_UPDATE_TRACE
+  append_residual<T, CH, P, ZC_UPD, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
+  UPD_TRACE(11);
+  if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
+#else
+  append_residual<T, CH, P, ZC_UPD, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
+#endif
 }
 
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
@@ -292,3 +325,16 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
 }
 
 }  // namespace ompb
+
+#ifdef OMP_UPDATE_TRACE
+extern "C" int omp_debug_update_trace(int k, unsigned long long* host16) {
+  // host16 == nullptr: arm the trace for iteration k (clears the sums); else read them back
+  if (!host16) {
+    unsigned long long z[16] = {};
+    cudaError_t e = cudaMemcpyToSymbol(g_upd_clk, z, sizeof(z));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_upd_trace_k, &k, sizeof(int));
+    return (int)e;
+  }
+  return (int)cudaMemcpyFromSymbol(host16, g_upd_clk, sizeof(unsigned long long) * 16);
+}
+#endif

@@ -239,7 +239,11 @@ struct TailSmem {
 template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false>
 __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
                                                 const float cst, const TailSmem& sm, const float* Fb,
-                                                float* Fs_append, const float4* rows_sm = nullptr) {
+                                                float* Fs_append, const float4* rows_sm = nullptr,
+                                                unsigned long long* trace_t0 = nullptr) {
+#ifdef OMP_UPDATE_TRACE
+  unsigned long long& upd_t0_ = *trace_t0;   // the caller's phase timer (diagnostic build only)
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q4 = (int)(a.Mp >> 2);
   float* w = sm.w;
@@ -277,14 +281,14 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       acc_z[c] = 0.f;
     }
     const int jl = min(j0 + ZC, k) - 1;   // last column of the group
-    int i = lane;
-    // long columns (F_k of a large S lives in L2): four rows' loads in flight, FMAs in the same order
-    for (; i + 96 <= jl; i += 128) {
+    // four rows' loads (predicated) in flight before their FMAs, which run in ascending row order:
+    // one round trip per 128 rows instead of one per 32 (F_k comes from L1/L2)
+    for (int i = lane; i <= jl; i += 128) {
       float cv[4][ZC], wv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int ii = i + 32 * q;
-        wv[q] = w[ii];
+        wv[q] = ii < k ? w[ii] : 0.f;
 #pragma unroll
         for (int c = 0; c < ZC; ++c) cv[q][c] = (ii <= j0 + c && j0 + c < k) ? col[c][ii] : 0.f;
       }
@@ -293,12 +297,6 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
 #pragma unroll
         for (int c = 0; c < ZC; ++c)
           if (i + 32 * q <= j0 + c && j0 + c < k) acc_z[c] = fmaf(cv[q][c], wv[q], acc_z[c]);
-    }
-    for (; i <= jl; i += 32) {
-      const float wi = w[i];
-#pragma unroll
-      for (int c = 0; c < ZC; ++c)
-        if (i <= j0 + c && j0 + c < k) acc_z[c] = fmaf(col[c][i], wi, acc_z[c]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)

@@ -19,6 +19,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
            "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
            "launch__grid_size", "launch__block_size", "sm__cycles_elapsed.avg.per_second"]
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12, "ms": 1e-3, "us": 1e-6, "ns": 1e-9,
@@ -104,7 +105,8 @@ def main():
             e.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0),
             e.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", 0),
             e.get("sm__throughput.avg.pct_of_peak_sustained_elapsed", 0),
-            e.get("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 0),
+            e.get("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                  e.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 0)),
             e.get("launch__registers_per_thread", 0)))
     open(os.path.join(prof, f"ncu_{tag}_{cfg}.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
