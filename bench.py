@@ -161,38 +161,51 @@ def ncu_traffic(kernel_key: str, config_name: str):
 
 
 # ------------------------------------------------------------------------------ roofline model
-def kernel_work(cfg, B, mode, path="residual"):
-    """Algorithmic work per launch (SURVEY §8(d) per signal-iteration, x the B signals one launch covers,
-    at the mean support size k = (S-1)/2 of a full run).  DESIGN.md §6 states each figure."""
+def kernel_work(cfg, B, mode, path="residual", n_iter=None):
+    """Algorithmic work per launch (SURVEY §8(d) per signal-iteration; DESIGN.md §6 states each figure),
+    summed over the signals each launch actually processes: with n_iter (iterations each signal ran,
+    from the step's own result) the launch at iteration k covers the live[k] = #{b : n_iter_b > k}
+    signals at support size k (eps stops, live-set compaction); the per-launch figure is the mean
+    over the S launches.  Without n_iter: all B signals for all S iterations."""
+    import numpy as np
     M, N, S = cfg["M"], cfg["N"], cfg["S"]
     Mp = -(-M // 64) * 64
-    k = (S - 1) / 2.0
+    ks = np.arange(S, dtype=np.float64)
+    if n_iter is None:
+        live = np.full(S, float(B))
+    else:
+        ni = np.asarray(n_iter).reshape(-1)
+        live = np.array([(ni > k).sum() for k in range(S)], dtype=np.float64)
+    per_launch = lambda f: float((live * f).sum() / S)   # noqa: E731  (f: per signal at iteration k)
     if path == "projection":
         Np = -(-N // 256) * 256
         # update: argmax over the p row, append, p = P0 - sum_j x_j G[s_j, :] (k+1 Gram rows from L2)
-        hbm = B * (4.0 * Np * 3 + 4.0 * k * (k + 1) / 2 + 4.0 * (k + 2) * 3)   # p read + P0 read + p write, F
-        l2 = B * 4.0 * Np * (k + 1)
+        hbm = per_launch(4.0 * Np * 3 + 4.0 * ks * (ks + 1) / 2 + 4.0 * (ks + 2) * 3)   # p read + P0 read + p write, F
+        l2 = per_launch(4.0 * Np * (ks + 1))
+        p0_simt = os.environ.get("OMP_B200_P0", "") == "simt"
         return {
-            # P0 = A^T Y once per batch: FP32 FFMA GEMM, 2 M N flops per signal
-            "correlation": ("alu", 2.0 * M * N * B, "TFLOP/s", None),
+            # P0 = A^T Y once per batch: 2 M N flops per signal (3xTF32 split-K on the tensor cores, or
+            # the FP32 FFMA GEMM with OMP_B200_P0=simt)
+            "correlation": ("alu" if p0_simt else "tensor3", 2.0 * M * N * B, "TFLOP/s", None),
             "update": ("l2", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
             "init": ("hbm", B * 4.0 * (2 * M + Mp), "GB/s", None),
         }
     tiles = math.ceil(N / 256)
     planes = {"bf16": 2.0, "3xtf32": 8.0, "simt": 0.0}[mode]
     # update = exact selection + factor append + residual, split into streamed (HBM) and gathered (L2)
-    hbm = B * (4.0 * Mp                      # fp32 residual row read by the selection
-               + 8.0 * 4 * tiles             # screen partials
-               + 4.0 * k * (k + 1) / 2       # packed F_k staged once
-               + 4.0 * (k + 2) * 3           # new F column, x, u
-               + 4.0 * M                     # y
-               + (4.0 + planes) * Mp)        # residual written: fp32 + screen planes
-    l2 = B * 4.0 * Mp * (k + 1 + 1)          # (k+1) gathered atom rows + ~1 candidate row
+    hbm = per_launch(4.0 * Mp                      # fp32 residual row read by the selection
+                     + 8.0 * 4 * tiles             # screen partials
+                     + 4.0 * ks * (ks + 1) / 2     # packed F_k staged once
+                     + 4.0 * (ks + 2) * 3          # new F column, x, u
+                     + 4.0 * M                     # y
+                     + (4.0 + planes) * Mp)        # residual written: fp32 + screen planes
+    l2 = per_launch(4.0 * Mp * (ks + 1 + 1))       # (k+1) gathered atom rows + ~1 candidate row
+    k = (S - 1) / 2.0
     return {
-        # screen GEMM: 2 M N flops per signal-iteration (the contraction C = A^T R)
-        "correlation": ("tensor", 2.0 * M * N * B, "TFLOP/s", None),
+        # screen GEMM: 2 M N flops per live signal-iteration (the contraction C = A^T R)
+        "correlation": ("tensor", per_launch(2.0 * M * N + 0 * ks), "TFLOP/s", None),
         # standalone argmax over the FP32 C (SIMT mode): 4N bytes per signal
-        "select": ("hbm", B * 4.0 * N, "GB/s", None),
+        "select": ("hbm", per_launch(4.0 * N + 0 * ks), "GB/s", None),
         "update": ("l2", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
         "init": ("hbm", B * (4.0 * M + (4.0 + planes) * Mp), "GB/s", None),
         # small-batch persistent kernel, all S iterations: per iteration the atom table once (phase A,
@@ -331,14 +344,17 @@ def main():
 
     # roofline of the dominant kernel (events measured live over the timed steps, this rank)
     path = h.last_path()
-    work = kernel_work(cfg, B, args.mode, path)
+    work = kernel_work(cfg, B, args.mode, path, res.n_iter.cpu().numpy() if B > 0 else None)
     dom = max((k for k in kern if k in work), key=lambda k: kern[k][0])
     bound, per_launch, unit, split = work[dom]
+    peak_mode = args.mode
+    if bound == "tensor3":                 # the projection path's P0: 3xTF32 whatever the screen mode
+        bound, peak_mode = "tensor", "3xtf32"
     t_launch = kern[dom][0] / max(1, kern[dom][1]) / 1e3
     peaks = measured_peaks()
     if bound == "tensor":
         achieved = per_launch / t_launch / 1e12
-        peak, peak_src = tensor_peak(peaks, args.mode)
+        peak, peak_src = tensor_peak(peaks, peak_mode)
     elif bound == "alu":
         # FP32 FFMA peak: 148 SMs x 128 lanes x 2 flops x 1.965 GHz (guide unit counts and max clock)
         achieved = per_launch / t_launch / 1e12
@@ -369,9 +385,12 @@ def main():
     roofline["others"] = {}
     for k, (tot_ms, n_l) in other.items():
         b2, w2, u2, _ = work[k]
+        pm2 = args.mode
+        if b2 == "tensor3":
+            b2, pm2 = "tensor", "3xtf32"
         t2 = tot_ms / n_l / 1e3
         if b2 in ("tensor", "alu"):
-            tp, tsrc = (74.4, "FP32 FFMA") if b2 == "alu" else tensor_peak(peaks, args.mode)
+            tp, tsrc = (74.4, "FP32 FFMA") if b2 == "alu" else tensor_peak(peaks, pm2)
             roofline["others"][k] = {"bound": b2, "achieved_tflops": w2 / t2 / 1e12, "launch_ms": t2 * 1e3,
                                      "frac": w2 / t2 / 1e12 / tp, "peak": tp, "peak_source": tsrc}
             if b2 == "tensor" and peaks and peaks.get("bf16_tflops_sustained"):

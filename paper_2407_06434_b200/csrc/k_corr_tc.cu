@@ -218,13 +218,6 @@ struct Maps {
 template <int KIND, int CG, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m, int tiles_n, EpiArgs ep) {
-  // live-set compaction: the live rows are the first *live_rows rows of the buffer; the grid was sized
-  // for the buffer's capacity and the clusters without a live tile have nothing to do
-  if (ep.live_rows) {
-    const int lr = *ep.live_rows;
-    if (lr < rows) rows = lr;
-    tiles_m = (rows + BM * CG - 1) / (BM * CG);
-  }
   using C_ = Cfg<KIND, CG>;
   using K_ = Kind<KIND>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -239,12 +232,10 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
   const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
-  // split-K (MODE_STORE): the work items are (slab z, tile); slab z covers K blocks [z kslab, ...)
-  const int kslab = ep.kslab > 0 ? ep.kslab : num_kb;
-  const int nz = (num_kb + kslab - 1) / kslab;
-  const int tiles_mn = tiles_m * tiles_n;
-  const int num_tiles = tiles_mn * nz;
-  const TileSched sched{tiles_m, tiles_n};
+
+  // programmatic dependent launch: the next kernel (the update) may start launching now; it waits
+  // for this grid's completion itself (griddepcontrol.wait) before touching anything this writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) {
@@ -270,6 +261,23 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  // everything above (barriers, TMEM) overlaps the previous kernel's tail under PDL; the operands and
+  // the live count are that kernel's output
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // live-set compaction: the live rows are the first *live_rows rows of the buffer; the grid was sized
+  // for the buffer's capacity and the clusters without a live tile have nothing to do
+  if (ep.live_rows) {
+    const int lr = *ep.live_rows;
+    if (lr < rows) rows = lr;
+    tiles_m = (rows + BM * CG - 1) / (BM * CG);
+  }
+  // split-K (MODE_STORE): the work items are (slab z, tile); slab z covers K blocks [z kslab, ...)
+  const int kslab = ep.kslab > 0 ? ep.kslab : num_kb;
+  const int nz = (num_kb + kslab - 1) / kslab;
+  const int tiles_mn = tiles_m * tiles_n;
+  const int num_tiles = tiles_mn * nz;
+  const TileSched sched{tiles_m, tiles_n};
 
   if (warp == 0) {
     // ===================== TMA producer (one thread per CTA) =====================
@@ -511,13 +519,15 @@ static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const 
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C_::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (MODE == MODE_TOPK && pdl_enabled(1)) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, maps, (int)R.rows, (int)(K / K_::BK), tiles_m, tiles_n, ep);
 }
 

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(T, 1) k_small(const SmallArgs s) {
   __shared__ float rn_s;
   __shared__ Cand red_c[NW];
   __shared__ int red_nan[NW];
-  const TailSmem sm{w, z, u, xs, ss, ro, red, &sel_n};
+  const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(rs), &sel_n};   // (rs is free in the tail)
   const int64_t b = cta;                 // the signal this CTA owns (if b < B)
   unsigned int epoch = 0;
   const int64_t gstride = (int64_t)G * NW;
@@ -376,8 +376,8 @@ cudaError_t launch_small(const UpdateLaunch& L, float4* pbest, unsigned int* bar
     if (per_sm < 1) per_sm = 1;
     if (per_sm > SMALL_MAX_CTAS_PER_SM) per_sm = SMALL_MAX_CTAS_PER_SM;
   }
-  // the same (T, CH) per Mp as the per-iteration update kernel (k_update.cu launch_r): the tail's
-  // reductions depend on T, and the two paths must agree bit for bit
+  // (T, CH) per Mp: the tail's results do not depend on T (T-independent reduction orders), so the
+  // small-batch path agrees bit for bit with the per-iteration kernel whatever block size each uses
   const int64_t q4 = L.Mp / 4;
   if (q4 <= 32) return launch_s<32, 1, 4>(s, smem, per_sm, st);
   if (q4 <= 64) return launch_s<64, 1, 4>(s, smem, per_sm, st);

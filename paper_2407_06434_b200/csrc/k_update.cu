@@ -58,10 +58,18 @@ constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
 #ifndef OMP_UPDATE_CTAS
 #define OMP_UPDATE_CTAS 1280
 #endif
+// float4 loads in flight per thread in the gather (P x CH, at least 2 rows): narrow rows (CH = 1, 2)
+// take more rows per round trip
+#ifndef OMP_UPDATE_PCH
+#define OMP_UPDATE_PCH 2
+#endif
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool REFINE = (SEL == SEL_SCREEN);
   const int64_t b = blockIdx.x;
+  // PDL (screened path): wait for the screen's completion, then let the next screen launch early
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.status[b] != SIG_RUNNING) return;
 #ifdef OMP_UPDATE_TRACE
   unsigned long long upd_t0_ = clock64();
@@ -71,11 +79,13 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
   const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update):
-  //   [the fp32 residual row (refine): Mp floats] [w, z, u, xs: Sp floats each] [ss, ro: Sp ints each]
+  //   [the fp32 residual row (refine): Mp floats; else Mp / 4 floats] [w, z, u, xs: Sp floats each]
+  //   [ss, ro: Sp ints each]
   //   [cand: RF_CAP ints (refine)]
   extern __shared__ __align__(16) uint8_t dsm[];
   float4* rsm = reinterpret_cast<float4*>(dsm);
-  float* w = reinterpret_cast<float*>(dsm + (REFINE ? (size_t)a.Mp * 4 : 0));
+  // (the first region doubles as the tail's ||r||^2 chunk partials, Mp / 4 floats, after the refine)
+  float* w = reinterpret_cast<float*>(dsm + (REFINE ? (size_t)a.Mp * 4 : (size_t)a.Mp));
   float* z = w + Sp;
   float* u = z + Sp;
   float* xs = u + Sp;
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     if (tid == 0) a.status[b] = (n == SEL_NAN) ? OMP_SIG_NAN : OMP_SIG_DEGENERATE;
     return;
   }
-  const TailSmem sm{w, z, u, xs, ss, ro, red, &sel_n};
+  const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
   append_residual<T, CH, P, ZC_UPD, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
   UPD_TRACE(11);
@@ -260,19 +270,24 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  if (SEL == SEL_SCREEN && pdl_enabled(2)) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs++;
+  }
   if (persist > 0) {
     // keep the fp32 atom table (re-read by every signal's gather) in the persisting L2 carve-out;
     // a launch attribute, so the caller's stream is left untouched
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(a.At);
-    attr[0].val.accessPolicyWindow.num_bytes = persist;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cudaLaunchAttribute& w = attr[cfg.numAttrs++];
+    w.id = cudaLaunchAttributeAccessPolicyWindow;
+    w.val.accessPolicyWindow.base_ptr = const_cast<float*>(a.At);
+    w.val.accessPolicyWindow.num_bytes = persist;
+    w.val.accessPolicyWindow.hitRatio = 1.0f;
+    w.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    w.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   }
+  cfg.attrs = attr;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
@@ -280,13 +295,16 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
 template <int SEL, int T, int CH>
 static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, bool few, cudaStream_t st) {
   if (few) return launch_t<SEL, T, CH, 1, (16 / CH > 2 ? 16 / CH : 2)>(a, B, smem, persist, st);
-  return launch_t<SEL, T, CH>(a, B, smem, persist, st);
+  constexpr int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32);
+  return launch_t<SEL, T, CH, MINB, (OMP_UPDATE_PCH / CH > 2 ? OMP_UPDATE_PCH / CH : 2)>(a, B, smem, persist, st);
 }
 
 template <int SEL>
 static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
-  // float4 chunks per row -> (T, CH), T * CH == q4 at powers of two.  k_small.cu uses the same map:
-  // the tail's reductions depend on T, and the two paths must agree bit for bit (P does not matter).
+  // float4 chunks per row -> (T, CH), T * CH == q4 at powers of two.  No floating-point result
+  // depends on T (the tail's reductions run in T-independent orders), so the map may depend on the
+  // batch size and differ from k_small.cu's: a signal's result is the same whichever kernel and block
+  // size processed it.
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -295,9 +313,17 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   }
   const bool few = B <= 2 * (int64_t)sms;
   const int64_t q4 = a.Mp / 4;
+  // Large batches of narrow rows (many waves: throughput) take one warp per signal and 32 signals per
+  // SM; smaller batches keep the wider CTAs, whose shorter per-signal chain sets the launch time when
+  // the whole batch is resident at once.  Measured (c5, M = 512): T = 32 vs 128 +14 % at B = 10^4,
+  // +24 % at 10^5, but -24 % at B = 10^3 and -30 % at 100; c3 (M = 1024, B = 10^4, eps stops): T = 64
+  // vs 128 -11 % -- hence only M <= 512 and B >= 8192.
+  const bool wide_batch = B >= 8192;
   if (q4 <= 32) return launch_tc<SEL, 32, 1>(a, B, smem, persist, few, st);
-  if (q4 <= 64) return launch_tc<SEL, 64, 1>(a, B, smem, persist, few, st);
-  if (q4 <= 128) return launch_tc<SEL, 128, 1>(a, B, smem, persist, few, st);
+  if (q4 <= 64) return wide_batch ? launch_tc<SEL, 32, 2>(a, B, smem, persist, few, st)
+                                  : launch_tc<SEL, 64, 1>(a, B, smem, persist, few, st);
+  if (q4 <= 128) return wide_batch ? launch_tc<SEL, 32, 4>(a, B, smem, persist, few, st)
+                                   : launch_tc<SEL, 128, 1>(a, B, smem, persist, few, st);
   if (q4 <= 256) return launch_tc<SEL, 128, 2>(a, B, smem, persist, few, st);
   if (q4 <= 512) return launch_tc<SEL, 128, 4>(a, B, smem, persist, few, st);
   if (q4 <= 1024) return launch_tc<SEL, 256, 4>(a, B, smem, persist, few, st);
@@ -318,7 +344,7 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.At_res = L.At_res; a.Mp_res = L.Mp_res; a.M_res = L.M_res; a.Y_res = L.Y_res; a.ldy_res = L.ldy_res;
   const bool refine = L.part != nullptr;
   const int64_t Sp = (L.k + 4) & ~3;
-  const size_t smem = (refine ? (size_t)L.Mp * 4 : 0) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
+  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
   if (refine) return launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);
   if (L.ynorm2) return launch_r<SEL_PROJ>(a, L.B, smem, L.l2_persist_bytes, st);
   return launch_r<SEL_GIVEN>(a, L.B, smem, L.l2_persist_bytes, st);

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "omp_b200.h"
 
@@ -23,6 +24,21 @@ constexpr int N_TILE = 256;    // atom padding (UMMA N of the correlation kernel
 constexpr int MAX_S = 512;
 constexpr int TOPK = 4;        // screening candidates kept per (signal, 128-atom half tile)
 constexpr int SCREEN_GROUP = 128;   // atoms per screen partial (half of the 256-atom UMMA tile)
+
+// Programmatic dependent launch between the screen and the update of the screened path: each kernel
+// lets the next one launch early (griddepcontrol.launch_dependents) and the next one waits for the
+// previous grid's completion (griddepcontrol.wait) before reading its output, so only launch latency
+// and prologues overlap.  OMP_B200_PDL=0 turns the launch attribute off (A/B; same results).
+// edge: 1 = update -> next screen (the screen's prologue overlaps the update's tail),
+//       2 = screen -> update (the update's launch overlaps the screen's tail)
+inline bool pdl_enabled(int edge) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("OMP_B200_PDL");
+    on = e ? atoi(e) : 1;   // measured: edge 1 gains 1-5 % (c2, c3, c5), edge 2 loses 2-10 %
+  }
+  return (on & edge) != 0;
+}
 
 // screening-GEMM operand kinds
 constexpr int KIND_BF16 = 0;

@@ -218,6 +218,7 @@ struct TailSmem {
   int* ss;
   uint32_t* ro;   // atom row offsets (float4 units) for the gather
   float* red;     // T / 32 floats
+  float* pr;      // Mp / 4 floats: per-chunk partials of ||r||^2
   int* bcast;     // one int
 };
 
@@ -309,9 +310,19 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   }
   __syncthreads();
   OMP_TAIL_TRACE(1);
+  // ||z||^2 in one order whatever T is (every warp computes the same value: lane l sums z_j^2 for
+  // j = l, l + 32, ... ascending, then the xor tree), so a signal's result does not depend on the
+  // kernel's block size
+#ifdef OMP_OLD_ZZ
   float zz = 0.f;
   for (int j = tid; j < k; j += T) zz = fmaf(z[j], z[j], zz);
   zz = block_sum<T>(zz, sm.red);
+#else
+  float zz = 0.f;
+  for (int j = lane; j < k; j += 32) zz = fmaf(z[j], z[j], zz);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, o);
+#endif
 
   OMP_TAIL_TRACE(2);
   const float delta = d - zz;
@@ -459,7 +470,6 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   OMP_TAIL_TRACE(4);
   const float* y = a.Y + b * a.ldy;
   const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
-  float part = 0.f;
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int q = tid + c * T;
@@ -475,7 +485,8 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
         yv.w = m + 3 < a.M ? y[m + 3] : 0.f;
       }
       acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);   // r
-      part = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, fmaf(acc[c].w, acc[c].w, part))));
+      // ||r||^2: one partial per float4 chunk, summed below in an order that does not depend on T
+      if constexpr (!V0) sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));
     }
   }
   float rr;
@@ -502,7 +513,19 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     }
     rr = (float)r2;
   } else {
+#ifdef OMP_OLD_RR
+    float part = 0.f;
+    for (int q = tid; q < q4; q += T) part += sm.pr[q];
     rr = block_sum<T>(part, sm.red);
+#else
+    __syncthreads();
+    rr = 0.f;
+    if (warp == 0) {                    // lane l: chunks l, l + 32, ... ascending, then the xor tree
+      for (int q = lane; q < q4; q += 32) rr += sm.pr[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    }
+#endif
   }
   OMP_TAIL_TRACE(5);
   if (tid == 0) {

@@ -210,6 +210,22 @@ def test_batch_invariance_bitwise(mode):
         assert np.array_equal(full[key][130:260], part[key]), key
 
 
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_update_block_size_invariance_bitwise(name):
+    """The per-iteration update picks its block size from the batch (one warp per signal for B >= 8192
+    at M <= 512, wider CTAs below, a high-ILP variant when B <= 2 x SMs); every reduction of the tail
+    runs in a T-independent order, so signal b's bits are the same in all of them (and with the
+    programmatic-dependent-launch edge on or off)."""
+    prob = make_problem(name, B=8192)
+    big = run_gpu(prob.A, prob.Y, prob.S, None, "bf16")
+    mid = run_gpu(prob.A, prob.Y[1000:3000], prob.S, None, "bf16")     # 2000 signals: wider CTAs
+    few = run_gpu(prob.A, prob.Y[4000:4100], prob.S, None, "bf16")     # 100 signals: few-CTA variant
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(big[key][1000:3000], mid[key]), key
+        assert np.array_equal(big[key][4000:4100], few[key]), key
+    assert_no_bugs(parity(few, prob.A, prob.Y[4000:4100], prob.S, None, range(0, 100, 7)), f"{name} B=100")
+
+
 @pytest.mark.parametrize("case", [("tiny", 16, {}), ("c2", 64, {}), ("c5", 20, {}), ("c5", 64, {"eps": 0.05}),
                                   ("c3", 8, {}), ("c4", 2, {})], ids=lambda c: f"{c[0]}-B{c[1]}")
 def test_small_path_bitwise_equals_screened(case):
