@@ -44,17 +44,35 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Compile every translation unit to an object in parallel (one nvcc per .cu), then link the
+    shared library.  `defines` / `out`: diagnostic builds (e.g. -DOMP_UPDATE_TRACE into another .so)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+    lib = out or LIB
+    if not force and out is None and not defines and up_to_date():
+        return lib
     cu = [s for s in sources() if s.endswith(".cu")]
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *cu]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory(prefix="omp_b200_build_") as td:
+        objs = [os.path.join(td, os.path.basename(c)[:-3] + ".o") for c in cu]
+        cmds = [[nvcc(), *flags, *defines, "-I", INCLUDE, "-I", CSRC, "-c", c, "-o", o] for c, o in zip(cu, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), flush=True)
+        workers = max(1, min(len(cmds), os.cpu_count() or 1))
+        with ThreadPoolExecutor(workers) as ex:
+            for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+                if r.returncode != 0:
+                    sys.stderr.write(r.stdout + r.stderr)
+                    raise subprocess.CalledProcessError(r.returncode, r.args)
+        tmp = lib + ".tmp"
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

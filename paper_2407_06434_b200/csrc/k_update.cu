@@ -41,14 +41,16 @@ __device__ unsigned long long g_upd_clk[16];
 namespace ompb {
 
 constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N atoms)
-#ifndef OMP_UPDATE_ZC
-#define OMP_UPDATE_ZC 2
-#endif
-constexpr int ZC_UPD = OMP_UPDATE_ZC;   // columns per warp in z = F^T w (interleaving only)
+constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared memory
+// columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
+// cost registers and lose at c4 and at c5 B = 10^5)
+template <int T>
+constexpr int zc_of() { return 2; }
 
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
 constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
+constexpr int SEL_SCREEN_FSM = 3;   // SEL_SCREEN with the packed F_k staged in shared memory
 
 // P: atom rows in flight per thread in the gather (2 at 8 CTAs per SM; more when the batch leaves
 // the SMs nearly empty and one CTA's memory parallelism is all a signal gets)
@@ -65,7 +67,8 @@ constexpr int SEL_GIVEN = 0, SEL_SCREEN = 1, SEL_PROJ = 2;
 #endif
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
-  constexpr bool REFINE = (SEL == SEL_SCREEN);
+  constexpr bool REFINE = (SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM);
+  constexpr bool FSM = (SEL == SEL_SCREEN_FSM);   // compile-time, so F's address space is known
   const int64_t b = blockIdx.x;
   // PDL (screened path): wait for the screen's completion, then let the next screen launch early
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -80,7 +83,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update):
   //   [the fp32 residual row (refine): Mp floats; else Mp / 4 floats] [w, z, u, xs: Sp floats each]
-  //   [ss, ro: Sp ints each]
+  //   [ss, ro: Sp ints each] [cand: RF_CAP ints (refine)] [F_k packed (fsm)]
   //   [cand: RF_CAP ints (refine)]
   extern __shared__ __align__(16) uint8_t dsm[];
   float4* rsm = reinterpret_cast<float4*>(dsm);
@@ -111,13 +114,23 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     const float4* r4g = reinterpret_cast<const float4*>(a.R32in + (int64_t)cur_slot * a.Mp);
     for (int q = tid; q < q4; q += T) cp_async16(&rsm[q], r4g + q);
   }
+  // a small packed F_k (fsm: decided at launch) goes to shared memory too: the column dots z = F^T w
+  // and the row sweeps F z, F u then read shared memory instead of dependent L2 round trips
+  float* Fs = reinterpret_cast<float*>(cand + (REFINE ? RF_CAP : 0));
+  if constexpr (FSM) {
+    const int f4 = (k * (k + 1) / 2 + 3) >> 2;          // within the row: ldf >= S(S+1)/2 rounded to 4
+    const float4* fg = reinterpret_cast<const float4*>(a.F + b * a.ldf);
+    for (int q = tid; q < f4; q += T) cp_async16(reinterpret_cast<float4*>(Fs) + q, fg + q);
+  }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  {
+  if constexpr (!FSM) {
     const char* fp = reinterpret_cast<const char*>(a.F + b * a.ldf);
     // (only while F_k fits L1 comfortably; a large one is read from L2 with loads in flight instead)
     const uint32_t fbytes = (uint32_t)min((int64_t)k * (k + 1) / 2 * 4, (int64_t)64 * 1024);
     for (uint32_t o = (uint32_t)tid * 128u; o < fbytes; o += (uint32_t)T * 128u)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
+  }
+  {
     const char* yp = reinterpret_cast<const char*>(a.Y + b * a.ldy);
     for (int64_t o = (int64_t)tid * 128; o < a.M * 4; o += (int64_t)T * 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
@@ -247,11 +260,11 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, ZC_UPD, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
+  append_residual<T, CH, P, zc_of<T>(), SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
 #else
-  append_residual<T, CH, P, ZC_UPD, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, zc_of<T>(), SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 
@@ -271,7 +284,7 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  if (SEL == SEL_SCREEN && pdl_enabled(2)) {
+  if ((SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM) && pdl_enabled(2)) {
     attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs++;
@@ -344,8 +357,14 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.At_res = L.At_res; a.Mp_res = L.Mp_res; a.M_res = L.M_res; a.Y_res = L.Y_res; a.ldy_res = L.ldy_res;
   const bool refine = L.part != nullptr;
   const int64_t Sp = (L.k + 4) & ~3;
-  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0);
-  if (refine) return launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);
+  // F_k staged in shared memory while it is small and the batch is latency-bound (< 8192 signals);
+  // the big batches keep their occupancy (measured: c2, c5 B <= 10^3)
+  const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) & ~3;
+  a.fsm = (refine && fk * 4 <= kFsmMaxBytes && L.B < 8192) ? 1 : 0;
+  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0) +
+                      (a.fsm ? (size_t)fk * 4 : 0);
+  if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)
+                           : launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);
   if (L.ynorm2) return launch_r<SEL_PROJ>(a, L.B, smem, L.l2_persist_bytes, st);
   return launch_r<SEL_GIVEN>(a, L.B, smem, L.l2_persist_bytes, st);
 }

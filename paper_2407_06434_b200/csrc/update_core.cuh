@@ -33,6 +33,7 @@ namespace ompb {
 
 struct UpdateArgs {
   int32_t k, S;
+  int32_t fsm;          // k_update: the packed F_k is staged in shared memory
   float eps;
   int64_t N, M, Mp;
   // selection inputs
@@ -282,14 +283,14 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       acc_z[c] = 0.f;
     }
     const int jl = min(j0 + ZC, k) - 1;   // last column of the group
-    // four rows' loads (predicated) in flight before their FMAs, which run in ascending row order:
-    // one round trip per 128 rows instead of one per 32 (F_k comes from L1/L2)
-    for (int i = lane; i <= jl; i += 128) {
+    int i = lane;
+    // long columns (F_k of a large S lives in L2): four rows' loads in flight, FMAs in the same order
+    for (; i + 96 <= jl; i += 128) {
       float cv[4][ZC], wv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int ii = i + 32 * q;
-        wv[q] = ii < k ? w[ii] : 0.f;
+        wv[q] = w[ii];
 #pragma unroll
         for (int c = 0; c < ZC; ++c) cv[q][c] = (ii <= j0 + c && j0 + c < k) ? col[c][ii] : 0.f;
       }
@@ -298,6 +299,12 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
 #pragma unroll
         for (int c = 0; c < ZC; ++c)
           if (i + 32 * q <= j0 + c && j0 + c < k) acc_z[c] = fmaf(cv[q][c], wv[q], acc_z[c]);
+    }
+    for (; i <= jl; i += 32) {
+      const float wi = w[i];
+#pragma unroll
+      for (int c = 0; c < ZC; ++c)
+        if (i <= j0 + c && j0 + c < k) acc_z[c] = fmaf(col[c][i], wi, acc_z[c]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -310,19 +317,18 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   }
   __syncthreads();
   OMP_TAIL_TRACE(1);
-  // ||z||^2 in one order whatever T is (every warp computes the same value: lane l sums z_j^2 for
-  // j = l, l + 32, ... ascending, then the xor tree), so a signal's result does not depend on the
-  // kernel's block size
-#ifdef OMP_OLD_ZZ
-  float zz = 0.f;
-  for (int j = tid; j < k; j += T) zz = fmaf(z[j], z[j], zz);
-  zz = block_sum<T>(zz, sm.red);
-#else
-  float zz = 0.f;
-  for (int j = lane; j < k; j += 32) zz = fmaf(z[j], z[j], zz);
+  // ||z||^2 in one order whatever T is: warp 0's lane l sums z_j^2 for j = l, l + 32, ... ascending,
+  // then the xor tree; one barrier broadcasts it.  So a signal's result does not depend on the
+  // kernel's block size.
+  if (warp == 0) {
+    float v = 0.f;
+    for (int j = lane; j < k; j += 32) v = fmaf(z[j], z[j], v);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, o);
-#endif
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sm.red[0] = v;
+  }
+  __syncthreads();
+  const float zz = sm.red[0];
 
   OMP_TAIL_TRACE(2);
   const float delta = d - zz;
@@ -513,11 +519,6 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     }
     rr = (float)r2;
   } else {
-#ifdef OMP_OLD_RR
-    float part = 0.f;
-    for (int q = tid; q < q4; q += T) part += sm.pr[q];
-    rr = block_sum<T>(part, sm.red);
-#else
     __syncthreads();
     rr = 0.f;
     if (warp == 0) {                    // lane l: chunks l, l + 32, ... ascending, then the xor tree
@@ -525,7 +526,6 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
     }
-#endif
   }
   OMP_TAIL_TRACE(5);
   if (tid == 0) {

@@ -21,9 +21,7 @@ PHASES = {0: "partials+cand list", 1: "wait rows", 2: "refine dots", 4: "w (Gram
 
 def build():
     from paper_2407_06434_b200 import build as b
-    cu = [s for s in b.sources() if s.endswith(".cu")]
-    cmd = [b.nvcc(), *b.NVCC_FLAGS, "-DOMP_UPDATE_TRACE", "-I", b.INCLUDE, "-I", b.CSRC, "-o", LIB, *cu]
-    subprocess.run(cmd, check=True)
+    b.build(defines=["-DOMP_UPDATE_TRACE"], out=LIB)
 
 
 def main():
