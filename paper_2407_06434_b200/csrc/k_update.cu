@@ -40,7 +40,10 @@ __device__ unsigned long long g_upd_clk[16];
 
 namespace ompb {
 
-constexpr int RF_CAP = 512;   // explicit candidate list capacity (beyond: all N atoms)
+#ifndef OMP_RF_CAP
+#define OMP_RF_CAP 512
+#endif
+constexpr int RF_CAP = OMP_RF_CAP;   // explicit candidate list capacity (beyond: all N atoms)
 constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared memory
 // columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
 // cost registers and lose at c4 and at c5 B = 10^5)
@@ -360,7 +363,11 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   // F_k staged in shared memory while it is small and the batch is latency-bound (< 8192 signals);
   // the big batches keep their occupancy (measured: c2, c5 B <= 10^3)
   const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) & ~3;
+#ifdef OMP_FSM_ALL_B
+  a.fsm = (refine && fk * 4 <= kFsmMaxBytes) ? 1 : 0;
+#else
   a.fsm = (refine && fk * 4 <= kFsmMaxBytes && L.B < 8192) ? 1 : 0;
+#endif
   const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0) +
                       (a.fsm ? (size_t)fk * 4 : 0);
   if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)
