@@ -194,6 +194,14 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     asm volatile("cp.async.wait_all;" ::: "memory");   // residual row (and ss, u) landed
     full = __syncthreads_or(full);
     UPD_TRACE(1);
+#ifdef OMP_UPDATE_TRACE
+    if (tid == 0 && a.k == g_upd_trace_k) {   // candidate statistics: sum, > 16, > 128, full fallback
+      atomicAdd(&g_upd_clk[12], (unsigned long long)min(ncand, RF_CAP));
+      if (ncand > 16) atomicAdd(&g_upd_clk[13], 1ull);
+      if (ncand > 128) atomicAdd(&g_upd_clk[14], 1ull);
+      if (full) atomicAdd(&g_upd_clk[3], 1ull);
+    }
+#endif
     Cand best{-1.f, 0x7fffffff, 0.f};
     bool nan_c = false;
     const int count = full ? (int)a.N : min(ncand, RF_CAP);
@@ -363,11 +371,9 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   // F_k staged in shared memory while it is small and the batch is latency-bound (< 8192 signals);
   // the big batches keep their occupancy (measured: c2, c5 B <= 10^3)
   const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) & ~3;
-#ifdef OMP_FSM_ALL_B
-  a.fsm = (refine && fk * 4 <= kFsmMaxBytes) ? 1 : 0;
-#else
-  a.fsm = (refine && fk * 4 <= kFsmMaxBytes && L.B < 8192) ? 1 : 0;
-#endif
+  // (large batches: only the one-warp-per-signal variant of narrow rows, M <= 512, gains: c5 B = 10^4
+  // +5 %; at c4 it cost 0.5 %)
+  a.fsm = (refine && fk * 4 <= kFsmMaxBytes && (L.B < 8192 || L.Mp <= 512)) ? 1 : 0;
   const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0) +
                       (a.fsm ? (size_t)fk * 4 : 0);
   if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)

@@ -22,7 +22,10 @@ constexpr float TAU_F = 1e-5f;
 constexpr int K_TILE = 64;     // K padding of every plane (a 128-byte bf16 TMA/UMMA row)
 constexpr int N_TILE = 256;    // atom padding (UMMA N of the correlation kernel)
 constexpr int MAX_S = 512;
-constexpr int TOPK = 4;        // screening candidates kept per (signal, 128-atom half tile)
+#ifndef OMP_TOPK
+#define OMP_TOPK 4
+#endif
+constexpr int TOPK = OMP_TOPK;   // screening candidates kept per (signal, 128-atom half tile)
 constexpr int SCREEN_GROUP = 128;   // atoms per screen partial (half of the 256-atom UMMA tile)
 
 // Programmatic dependent launch between the screen and the update of the screened path: each kernel
