@@ -47,8 +47,7 @@ constexpr int RF_CAP = OMP_RF_CAP;   // explicit candidate list capacity (beyond
 constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared memory
 // columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
 // cost registers and lose at c4 and at c5 B = 10^5)
-template <int T>
-constexpr int zc_of() { return 2; }
+constexpr int kZC = 2;
 
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
@@ -271,11 +270,11 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, zc_of<T>(), SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
+  append_residual<T, CH, P, kZC, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
 #else
-  append_residual<T, CH, P, zc_of<T>(), SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, kZC, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 
@@ -371,9 +370,11 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   // F_k staged in shared memory while it is small and the batch is latency-bound (< 8192 signals);
   // the big batches keep their occupancy (measured: c2, c5 B <= 10^3)
   const int64_t fk = ((int64_t)L.k * (L.k + 1) / 2 + 3) & ~3;
-  // (large batches: only the one-warp-per-signal variant of narrow rows, M <= 512, gains: c5 B = 10^4
-  // +5 %; at c4 it cost 0.5 %)
-  a.fsm = (refine && fk * 4 <= kFsmMaxBytes && (L.B < 8192 || L.Mp <= 512)) ? 1 : 0;
+  // (large batches: only up to M = 1024 -- c5 B = 10^4 +2..5 %, c3 B = 3 x 10^4 +1 %; at c4 it cost 0.5 %)
+#ifndef OMP_FSM_MP_MAX
+#define OMP_FSM_MP_MAX 1024
+#endif
+  a.fsm = (refine && fk * 4 <= kFsmMaxBytes && (L.B < 8192 || L.Mp <= OMP_FSM_MP_MAX)) ? 1 : 0;
   const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0) +
                       (a.fsm ? (size_t)fk * 4 : 0);
   if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)
