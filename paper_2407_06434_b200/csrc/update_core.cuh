@@ -132,19 +132,6 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 
 template <int T>
-__device__ __forceinline__ float block_sum(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  float r = 0.f;
-#pragma unroll
-  for (int w = 0; w < T / 32; ++w) r += red[w];
-  return r;
-}
-
-template <int T>
 __device__ __forceinline__ double block_sum_d(double v) {
   __shared__ double redd[T / 32];
 #pragma unroll
