@@ -210,6 +210,29 @@ def test_batch_invariance_bitwise(mode):
         assert np.array_equal(full[key][130:260], part[key]), key
 
 
+@pytest.mark.parametrize("mode", ["bf16", "3xtf32"])
+def test_overflowing_screen_groups_find_the_exact_argmax(mode):
+    """Many exact ties inside one 128-atom screen group (12 orthonormal atoms with equal coefficients):
+    more in-window entries than the screen keeps, so the group is flagged as overflowing and the update
+    must still land on the exact FP32 argmax.  The small-batch kernel evaluates every atom exactly (same
+    dot order, no screen), so the two paths must agree bit for bit."""
+    rng = np.random.default_rng(11)
+    M = 256
+    Q1 = np.linalg.qr(rng.standard_normal((M, M)))[0]
+    Q2 = np.linalg.qr(rng.standard_normal((M, M)))[0]
+    A = np.concatenate([Q1, Q2], axis=1).astype(np.float32)          # N = 512: four 128-atom groups
+    Y = np.zeros((4, M), dtype=np.float32)
+    for b, start in enumerate((0, 3, 40, 100)):                      # 12 tied atoms inside group 0
+        Y[b] = A[:, start:start + 12].astype(np.float64).sum(axis=1).astype(np.float32)
+    scr = run_gpu(A, Y, 12, None, mode)
+    small = run_gpu(A, Y, 12, None, "small")
+    assert scr["path"] == "residual" and small["path"] == "small"
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(scr[key], small[key]), key
+    for b, start in enumerate((0, 3, 40, 100)):                      # every tied atom is recovered
+        assert set(scr["support"][b].tolist()) == set(range(start, start + 12))
+
+
 @pytest.mark.parametrize("name", ["c2", "c5"])
 def test_update_block_size_invariance_bitwise(name):
     """The per-iteration update picks its block size from the batch (one warp per signal for B >= 8192
