@@ -124,6 +124,16 @@ ompStatus_t ompDensify(ompHandle_t handle, const float* X, int64_t ldx, const in
 ompStatus_t ompCorrelate(ompHandle_t handle, const float* R, int64_t B, int64_t ldr, float* C,
                          int64_t ldc, void* stream);
 
+/* ompScreeningWindow — the screen's candidate window W / ||r|| for a correlation mode and a
+ *   dictionary of M rows (host-only arithmetic, no device work; callable without a GPU).
+ *   In a tensor-core mode the exact selection n* = argmax |<r, a_n>| / ||a_n||
+ *   re-evaluates in FP32 every atom whose screened value is within W ||r|| of the screen's
+ *   maximum; W = 2.5 (c0 + c0'), c0 the rigorous per-element bound of the screen
+ *   (bf16: 2^-7 + 2^-16 + 2^-22 + Mp 2^-23; 3xTF32: 2^-20 + 2^-22 + 3 Mp 2^-23) and c0' that of
+ *   the FP32 re-evaluation, (Mp/32 + 8) 2^-23; Mp = M rounded up to 64.
+ *   Returns -1 for M < 1 or a mode without a screen (OMP_CORR_FP32_SIMT) or an unknown mode.  */
+float ompScreeningWindow(int corr_mode, int64_t M);
+
 /* ompGetGram — copy G = A^T A (N x N row-major, ldg >= N) from the handle.                */
 ompStatus_t ompGetGram(ompHandle_t handle, float* G, int64_t ldg, void* stream);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
     "ompDensify": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int32,
                            c_void_p, c_int64, c_void_p]),
     "ompCorrelate": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
+    "ompScreeningWindow": (c_float, [c_int, c_int64]),
     "ompGetGram": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "ompGetFactor": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "ompProfileEnable": (c_int, [c_void_p, c_int]),

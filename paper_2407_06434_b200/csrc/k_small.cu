@@ -21,6 +21,8 @@
 // signal (b mod G), so it never crosses SMs.  Data that does (residual rows, statuses, partials)
 // is written before a barrier and read after it with ld.global.cg (L2), never from L1.
 #include <math.h>
+
+#include <atomic>
 #include <stdlib.h>
 
 #include "omp_internal.cuh"
@@ -284,11 +286,17 @@ template <int T, int CH, int KC>
 static cudaError_t launch_s(SmallArgs s, size_t smem0, int ctas_per_sm, cudaStream_t st) {
   auto kern = k_small<T, CH, KC>;
   constexpr size_t kMaxSmem = 200 * 1024;
-  static bool opted = false;
-  if (!opted) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
-    if (e != cudaSuccess) return e;
-    opted = true;
+  // (a function attribute is per device: one opt-in per device this process launches on)
+  static std::atomic<uint64_t> opted{0};
+  {
+    int dev_ = 0;
+    if (cudaGetDevice(&dev_) != cudaSuccess) return cudaGetLastError();
+    const uint64_t bit = 1ull << (dev_ & 63);
+    if (!(opted.load(std::memory_order_acquire) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+      if (e != cudaSuccess) return e;
+      opted.fetch_or(bit, std::memory_order_acq_rel);
+    }
   }
   int dev = 0, sms = 0, occ = 0;
   cudaError_t e = cudaGetDevice(&dev);

@@ -17,6 +17,8 @@
 // Every live signal is at the same k (= iteration), so k is a kernel argument.  Finished signals
 // return at once (capture-and-continue).
 #include <math.h>
+
+#include <atomic>
 #include <stdlib.h>
 
 #ifdef OMP_UPDATE_TRACE
@@ -282,11 +284,17 @@ template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPD
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
   auto kern = k_update<SEL, T, CH, MINB, P>;
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
-  static bool opted = false;
-  if (!opted) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e != cudaSuccess) return e;
-    opted = true;
+  // (a function attribute is per device: one opt-in per device this process launches on)
+  static std::atomic<uint64_t> opted{0};
+  {
+    int dev_ = 0;
+    if (cudaGetDevice(&dev_) != cudaSuccess) return cudaGetLastError();
+    const uint64_t bit = 1ull << (dev_ & 63);
+    if (!(opted.load(std::memory_order_acquire) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (e != cudaSuccess) return e;
+      opted.fetch_or(bit, std::memory_order_acq_rel);
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)B);

@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <climits>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -48,6 +49,7 @@ struct ompHandle_st {
   int mode = OMP_CORR_3XTF32;
   float window = 0.f;      // screening window / ||r|| (tensor-core modes), DESIGN.md §5
   size_t l2_persist = 0;   // bytes of At under a persisting L2 access-policy window (0: off)
+  bool persist_ref = false; // this handle holds a reference on the device's persisting-L2 limit
   // dictionary (owned): FP32 copy of A^T (Np x Mp), the screen's plane(s), 1/||a_n||, Gram
   float *At = nullptr, *At_hi = nullptr, *At_lo = nullptr, *norm = nullptr, *inv_norm = nullptr, *G = nullptr;
   uint16_t* Ab = nullptr;  // bf16 plane
@@ -115,6 +117,33 @@ struct ompHandle_st {
 
 static thread_local int64_t g_create_detail = 0;
 
+// Live handles per device holding the persisting-L2 limit, and the limit found when the first was
+// created (restored when the last goes).  Devices beyond kMaxDevices keep the limit untouched.
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_persist_mu;
+int g_persist_count[kMaxDevices] = {};
+size_t g_persist_saved[kMaxDevices] = {};
+
+bool persist_acquire(int device) {
+  if (device < 0 || device >= kMaxDevices) return false;
+  std::lock_guard<std::mutex> lk(g_persist_mu);
+  if (g_persist_count[device]++ == 0 &&
+      cudaDeviceGetLimit(&g_persist_saved[device], cudaLimitPersistingL2CacheSize) != cudaSuccess)
+    g_persist_saved[device] = 0;
+  return true;
+}
+
+void persist_release(int device) {   // with `device` current
+  std::lock_guard<std::mutex> lk(g_persist_mu);
+  if (--g_persist_count[device] == 0) {
+    cudaCtxResetPersistingL2Cache();   // demote the lines this library marked persisting
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_persist_saved[device]);
+    cudaGetLastError();
+  }
+}
+}  // namespace
+
 namespace {
 
 struct DevGuard {
@@ -181,12 +210,18 @@ static Operand resid_operand(const ompHandle_t h, int64_t B, int buf) {
 }
 
 // rigorous screening bound c0 (|c~ - c| <= c0 ||a|| ||r||) + the FP32 re-evaluation bound,
-// doubled (both sides of the window) and padded by 25% for the FP32 norms
+// doubled (both sides of the window) and padded by 25% for the FP32 norms.
+// bf16: each operand is rounded to nearest with an 8-bit significand, unit roundoff u = 2^-8 (the
+// normalised atom also carries the FP32 scaling a_n * (1/||a_n||): 2 x 2^-24 more), so one product
+// is off by at most (1 + u + 2^-23)(1 + u) - 1 <= 2^-7 + 2^-16 + 2^-22; the product of two bf16
+// values is exact in FP32, and the accumulator truncates at most once per product (K 2^-23).
+// 3xTF32: hi = rna_tf32(x), lo = x - hi taken by the tensor core as tf32 (truncated: 2^-21 of x per
+// operand), the dropped lo * lo term 2^-22, three products per element into the accumulator.
 static float screening_window(int mode, int64_t Kp) {
   const double u23 = ldexp(1.0, -23);
   double c0;
   if (mode == OMP_CORR_3XTF32) c0 = ldexp(1.0, -20) + ldexp(1.0, -22) + 3.0 * (double)Kp * u23;
-  else c0 = ldexp(1.0, -8) + ldexp(1.0, -18) + (double)Kp * u23;   // bf16 operands
+  else c0 = ldexp(1.0, -7) + ldexp(1.0, -16) + ldexp(1.0, -22) + (double)Kp * u23;   // bf16 operands
   const double c_refine = ((double)Kp / 32.0 + 8.0) * u23;
   return (float)(2.0 * (c0 + c_refine) * 1.25);
 }
@@ -270,14 +305,6 @@ static ompStatus_t ensure_small(ompHandle_t h) {
   if (!dalloc(h->pbest, (size_t)SMALL_MAX_B * sms * SMALL_MAX_CTAS_PER_SM) || !dalloc(h->gbar, 1)) {
     dfree(h->pbest);
     dfree(h->gbar);
-    dfree(h->P0);
-    dfree(h->P);
-    dfree(h->Pwork);
-    dfree(h->yy);
-    dfree(h->PAhi);
-    dfree(h->PAlo);
-    dfree(h->PYhi);
-    dfree(h->PYlo);
     cudaGetLastError();
     return OMP_ERR_NOMEM;
   }
@@ -302,8 +329,11 @@ static bool p0_on_tensor_cores() {
 // Automatic choice by a cost model per signal-iteration: the residual path pays the
 // screen (2 M N flops on the tensor cores) plus an M-wide gather of k + 2 atom rows; the projection
 // path pays an N-wide gather of k + 2 Gram rows plus, amortised over S, the FP32 GEMM P0 = A^T Y.
+// The projection path runs the update kernel over N-wide rows (Mp := Np), which supports Np <= 8192.
+static bool proj_supported(const ompHandle_t h) { return h->Np <= 8192; }
+
 static bool use_proj(ompHandle_t h, int64_t B, int32_t S) {
-  if (h->algo == OMP_ALGO_RESIDUAL || B == 0) return false;
+  if (h->algo == OMP_ALGO_RESIDUAL || B == 0 || !proj_supported(h)) return false;
   if (h->algo == OMP_ALGO_PROJECTION) return true;
   const double kk = S / 2.0 + 2.0, M = (double)h->M, N = (double)h->N;
   const double t_res = 2.0 * M * N / 1.4e15 + kk * (double)h->Mp * 4.0 / 2.0e13;
@@ -629,6 +659,7 @@ static ompStatus_t check_batch_args(ompHandle_t h, const void* Y, int64_t B, int
   if (ldx < S || lds < S) return OMP_ERR_INVALID_ARG;
   if (B > 0 && (!Y || !X || !support || !resid || !n_iter || !status)) return OMP_ERR_INVALID_ARG;
   if (h->Mp > 8192) return OMP_ERR_UNSUPPORTED;
+  if (h->algo == OMP_ALGO_PROJECTION && !proj_supported(h)) return OMP_ERR_UNSUPPORTED;   // N > 8192
   return OMP_OK;
 }
 
@@ -688,12 +719,15 @@ ompStatus_t ompDestroy(ompHandle_t h) {
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
     dfree(h->rslot); dfree(h->slot); dfree(h->live);
     dfree(h->nstar); dfree(h->cstar); dfree(h->part);
+    dfree(h->P0); dfree(h->P); dfree(h->Pwork); dfree(h->yy);
+    dfree(h->PAhi); dfree(h->PAlo); dfree(h->PYhi); dfree(h->PYlo);
     dfree(h->hY); dfree(h->hX); dfree(h->hres); dfree(h->hsup); dfree(h->hnit); dfree(h->hst);
     for (auto& r : h->prof_pending) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->persist_ref) persist_release(h->device);
   }
   delete h;
   return OMP_OK;
@@ -724,19 +758,22 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   h->mode = corr_mode;
   h->window = screening_window(corr_mode, h->Mp);
   {
-    // persisting-L2 carve-out for the fp32 atom table gathered by every signal (K4); only ever
-    // raises the device limit; OMP_B200_L2_PERSIST=0 disables it
+    // persisting-L2 carve-out for the fp32 atom table gathered by every signal (K4; +3 % at c4,
+    // profiles/ab/ab26); OMP_B200_L2_PERSIST=0 disables it.  The device limit is process state:
+    // the first live handle on a device records the caller's limit, handles only ever raise it, and
+    // the last one destroyed restores it (persist_acquire / persist_release)
     const char* env = getenv("OMP_B200_L2_PERSIST");
     int maxp = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
     const size_t want = (size_t)h->Np * h->Mp * sizeof(float);
-    if (!(env && env[0] == '0') && maxp > 0) {
+    if (!(env && env[0] == '0') && maxp > 0 && persist_acquire(device)) {
       size_t cur = 0;
       cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
       const size_t lim = want < (size_t)maxp ? want : (size_t)maxp;
       if (cur < lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
       cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
       h->l2_persist = cur < want ? cur : want;
+      h->persist_ref = true;
     }
     cudaGetLastError();
   }
@@ -917,6 +954,11 @@ ompStatus_t ompCorrelate(ompHandle_t h, const float* R, int64_t B, int64_t ldr, 
     e = cudaMemcpy2DAsync(C, ldc * sizeof(float), h->C, h->Np * sizeof(float), h->N * sizeof(float), B,
                           cudaMemcpyDeviceToDevice, st);
   return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
+}
+
+float ompScreeningWindow(int corr_mode, int64_t M) {
+  if (M < 1 || (corr_mode != OMP_CORR_BF16 && corr_mode != OMP_CORR_3XTF32)) return -1.f;
+  return screening_window(corr_mode, round_up(M, K_TILE));
 }
 
 ompStatus_t ompGetGram(ompHandle_t h, float* G, int64_t ldg, void* stream) {

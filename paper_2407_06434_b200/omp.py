@@ -54,12 +54,13 @@ class OMP:
         self.device = A.device
         self.mode = mode
         At = A.t()
-        if At.stride(1) != 1:
+        if At.stride(1) != 1 or (self.N > 1 and At.stride(0) < self.M):
             At = At.contiguous()      # column-major (atom-contiguous) layout the ABI takes; lda = At.stride(0)
         h = ctypes.c_void_p()
         st = _stream_ptr(stream, self.device)
+        lda = At.stride(0) if self.N > 1 else self.M
         rc = self.lib.ompCreate(ctypes.byref(h), self.device.index, At.data_ptr(), self.M, self.N,
-                                At.stride(0), MODES[mode], st)
+                                lda, MODES[mode], st)
         check(rc, "ompCreate", None)
         self.handle = h
 
@@ -88,9 +89,11 @@ class OMP:
             raise TypeError("Y must be a 2-D float32 CUDA tensor of shape (B, M)")
         if Y.shape[1] != self.M:
             raise ValueError(f"Y has {Y.shape[1]} measurements, dictionary has M={self.M}")
-        if Y.stride(1) != 1:
-            Y = Y.contiguous()
         B = Y.shape[0]
+        # rows must not overlap (an expanded Y has stride(0) = 0): the library reads B x ldy floats
+        if Y.stride(1) != 1 or (B > 1 and Y.stride(0) < self.M):
+            Y = Y.contiguous()
+        ldy = Y.stride(0) if B > 1 else self.M
         dev = self.device
         if out is None:
             out = OMPResult(torch.empty((B, S), dtype=torch.float32, device=dev),
@@ -99,7 +102,7 @@ class OMP:
                             torch.empty((B,), dtype=torch.int32, device=dev),
                             torch.empty((B,), dtype=torch.int32, device=dev))
         e = float("nan") if eps is None else float(eps)
-        rc = self.lib.ompBatch(self.handle, Y.data_ptr(), B, max(Y.stride(0), self.M), S, e,
+        rc = self.lib.ompBatch(self.handle, Y.data_ptr(), B, ldy, S, e,
                                out.X.data_ptr(), out.X.stride(0), out.support.data_ptr(),
                                out.support.stride(0), out.resid_norm.data_ptr(), out.n_iter.data_ptr(),
                                out.status.data_ptr(), _stream_ptr(stream, dev))
@@ -181,6 +184,12 @@ class OMP:
 
     def launch_count(self) -> int:
         return int(self.lib.ompGetLaunchCount(self.handle))
+
+
+def screening_window(mode: str, M: int) -> float:
+    """W / ||r||: the tensor-core screen's candidate window for a dictionary of M rows
+    (ompScreeningWindow; host arithmetic only, no GPU needed).  -1 for the SIMT mode."""
+    return float(_lib.load().ompScreeningWindow(MODES[mode], int(M)))
 
 
 def omp_batch(A, Y, S: int, eps: Optional[float] = None, mode: str = "bf16") -> OMPResult:

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "omp_b200.h")
 def declared_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:ompStatus_t|int64_t|int|const char\s*\*)\s*(\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:ompStatus_t|int64_t|int|float|const char\s*\*)\s*(\w+)\s*\(", text, flags=re.M)))
 
 
 @pytest.fixture(scope="module")

@@ -26,11 +26,12 @@ STATUS = {"MAXITER": MAXITER, "EPS": EPS, "DEGENERATE": DEGENERATE, "NAN": NAN}
 # ------------------------------------------------------------------ correlation GEMM (K1)
 def screening_bound(mode, K):
     """Rigorous |c~ - c| / (||a|| ||r||) of each correlation kernel: operand rounding
-    (bf16: 2 x 2^-9; 3xTF32: tf32-truncated lo terms + dropped lo*lo) plus at most one truncation
-    of the FP32 accumulator per product (K, or 3K for the three 3xTF32 products) times 2^-23."""
+    (bf16: round-to-nearest, unit roundoff 2^-8 per operand -> 2^-7 + 2^-16, plus 2^-22 for the FP32
+    normalisation of the atom; 3xTF32: tf32-truncated lo terms + dropped lo*lo) plus at most one
+    truncation of the FP32 accumulator per product (K, or 3K for the three 3xTF32 products) x 2^-23."""
     Kp = -(-K // 64) * 64
     if mode == "bf16":
-        return 2.0 ** -8 + 2.0 ** -18 + Kp * 2.0 ** -23
+        return 2.0 ** -7 + 2.0 ** -16 + 2.0 ** -22 + Kp * 2.0 ** -23
     if mode == "3xtf32":
         return 2.0 ** -20 + 2.0 ** -22 + 3 * Kp * 2.0 ** -23
     return 1e-6
@@ -233,6 +234,66 @@ def test_overflowing_screen_groups_find_the_exact_argmax(mode):
         assert set(scr["support"][b].tolist()) == set(range(start, start + 12))
 
 
+ADVERSARY_CASES = [(M, seed, swap) for M in (48, 64, 256, 1024) for seed in (0, 1) for swap in (False, True)]
+
+
+@pytest.mark.parametrize("mode", ["bf16", "3xtf32"])
+def test_screen_window_adversarial_rounding(mode):
+    """Two nearly tied atoms (FP32 gap 2e-5 relative, unflagged by the oracle) whose operands sit just
+    below / just above bf16 rounding midpoints (synth.adversarial; tests/test_screen_window.py shows
+    on the CPU that the bf16 screen then ranks the loser ahead by 0.0107 ||r||, more than the round-1
+    window 0.0098 ||r||, less than the rigorous 0.0196 ||r||).  16 copies per signal on the screened
+    path (small-batch limit 0), every decision against the oracle, bitwise against the small-batch
+    kernel (exact FP32 over all atoms)."""
+    from synth.adversarial import make_screen_adversary
+    for M, seed, swap in ADVERSARY_CASES:
+        A, y, _ = make_screen_adversary(M, seed, swap)
+        Y = np.repeat(y[None, :], 16, axis=0)
+        scr = run_gpu(A, Y, 2, None, mode)
+        small = run_gpu(A, Y, 2, None, "small")
+        assert scr["path"] == "residual" and small["path"] == "small"
+        win = 1 if swap else 0
+        assert np.all(scr["support"] == [win, 1 - win]), (M, seed, swap, scr["support"][0])
+        for key in ("support", "X", "resid", "n_iter", "status"):
+            assert np.array_equal(scr[key], small[key]), (M, seed, swap, key)
+        d = assert_no_bugs(parity(scr, A, Y, 2, None, range(2)), f"adversary {M}/{seed}/{swap}/{mode}")
+        assert d["counts"].get("exact", 0) == 2
+
+
+@pytest.mark.parametrize("mode", ["bf16", "3xtf32"])
+def test_refine_falls_back_to_all_atoms(mode):
+    """More than RF_CAP = 512 candidates inside the window: 600 exactly tied atoms (identity
+    dictionary, M = N = 1024, y = sum of 600 unit vectors) fill every 128-atom screen group past its
+    4 kept entries, so all 8 groups (1024 atoms) are candidates and the update re-evaluates all N
+    atoms.  Exact ties -> lowest index (reading R4): the selections are the tied atoms in ascending
+    order, every coefficient exactly 1, ||r||^2 = 600 - S exactly.  Then a random orthonormal
+    dictionary with the same structure (ties to ~1e-7, all inside the window): bitwise equal to the
+    small-batch kernel, which evaluates every atom exactly."""
+    M = N = 1024
+    S, B = 16, 16
+    rng = np.random.default_rng(5)
+    T = [np.sort(rng.choice(N, 600, replace=False)) for _ in range(B)]
+    A = np.eye(M, dtype=np.float32)
+    Y = np.zeros((B, M), dtype=np.float32)
+    for b in range(B):
+        Y[b, T[b]] = 1.0
+    scr = run_gpu(A, Y, S, None, mode)
+    small = run_gpu(A, Y, S, None, "small")
+    for b in range(B):
+        assert np.array_equal(scr["support"][b], T[b][:S]), b
+    assert np.all(scr["X"] == 1.0) and np.all(scr["status"] == MAXITER) and np.all(scr["n_iter"] == S)
+    assert np.all(scr["resid"] == np.float32(np.sqrt(600 - S)))
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(scr[key], small[key]), key
+    Q = np.linalg.qr(rng.standard_normal((M, M)))[0].astype(np.float32)
+    Yq = np.stack([Q[:, T[b]].astype(np.float64).sum(axis=1) for b in range(B)]).astype(np.float32)
+    scr = run_gpu(Q, Yq, S, None, mode)
+    small = run_gpu(Q, Yq, S, None, "small")
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(scr[key], small[key]), key
+    assert_no_bugs(parity(scr, Q, Yq, S, None, range(4)), f"orthonormal ties/{mode}")
+
+
 @pytest.mark.parametrize("name", ["c2", "c5"])
 def test_update_block_size_invariance_bitwise(name):
     """The per-iteration update picks its block size from the batch (one warp per signal for B >= 8192
@@ -424,3 +485,70 @@ def test_inverse_cholesky_state_identity():
         V = np.linalg.cholesky(A_k.T @ A_k)
         assert np.abs(Fd @ V.T - np.eye(S)).max() <= 5e-5
         np.testing.assert_allclose(u[b], Fd.T @ (A_k.T @ prob.Y[b].astype(np.float64)), atol=2e-5)
+
+
+def test_one_shot_c_abi_omp_batch():
+    """The north star's one-shot call omp_batch(A, Y, S, eps) -> X, support, ||r|| through ctypes with
+    device pointers (column-major A, lda = M; Y M x B, ldy = M), bitwise equal to the handle API."""
+    import ctypes
+    import torch
+    from paper_2407_06434_b200 import _lib
+    lib = _lib.load()
+    prob = make_problem("c3", B=300)
+    M, N, S, B = prob.M, prob.N, prob.S, prob.B
+    A = torch.from_numpy(np.ascontiguousarray(prob.A.T)).cuda()     # atom n at A + n * M
+    Y = torch.from_numpy(prob.Y).cuda()                               # signal b at Y + b * M
+    X = torch.empty((B, S), device="cuda")
+    sup = torch.empty((B, S), dtype=torch.int32, device="cuda")
+    res = torch.empty(B, device="cuda")
+    nit = torch.empty(B, dtype=torch.int32, device="cuda")
+    st = torch.empty(B, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = lib.omp_batch(A.data_ptr(), M, N, Y.data_ptr(), B, S, ctypes.c_float(eps32(prob.eps)), X.data_ptr(),
+                       sup.data_ptr(), res.data_ptr(), nit.data_ptr(), st.data_ptr(), stream)
+    assert rc == 0
+    want = run_gpu(prob.A, prob.Y, S, prob.eps, "auto")
+    for key, got in (("X", X), ("support", sup), ("resid", res), ("n_iter", nit), ("status", st)):
+        assert np.array_equal(got.cpu().numpy(), want[key]), key
+    assert lib.omp_batch(A.data_ptr(), M, N, Y.data_ptr(), B, 0, ctypes.c_float(-1.0), X.data_ptr(), sup.data_ptr(),
+                         res.data_ptr(), nit.data_ptr(), st.data_ptr(), stream) == 1     # S = 0
+
+
+def test_expanded_and_overlapping_inputs_are_copied():
+    """Y = y.expand(B, M) (row stride 0) must not make the library read B x M floats of a buffer that
+    holds M: the binding copies such views; the result equals the contiguous batch bit for bit."""
+    import torch
+    from paper_2407_06434_b200 import OMP
+    prob = make_problem("c2", B=1)
+    with OMP(torch.from_numpy(prob.A).cuda()) as h:
+        y = torch.from_numpy(prob.Y[0]).cuda()
+        got = h.batch(y.expand(40, prob.M), prob.S)
+        want = h.batch(y.expand(40, prob.M).contiguous(), prob.S)
+        for key in ("X", "support", "resid_norm", "n_iter", "status"):
+            assert torch.equal(getattr(got, key), getattr(want, key)), key
+        one = h.batch(y.expand(1, prob.M), prob.S)        # B = 1: any row stride is fine
+        assert torch.equal(one.support, want.support[:1])
+
+
+def test_projection_needs_n_at_most_8192():
+    """The projection path runs N-wide rows (N <= 8192): AUTO picks the residual path for a tall
+    dictionary with N > 8192 (M = 8064, N = 9000 would favour projection), and an explicit projection
+    request fails with OMP_ERR_UNSUPPORTED before any launch, leaving the handle usable."""
+    import torch
+    from paper_2407_06434_b200 import OMP, OmpError
+    M, N, S, B = 8064, 9000, 4, 16
+    A = make_dictionary(M, N, 31)
+    Y = make_signals(A, range(B), 31, S)
+    with OMP(torch.from_numpy(A).cuda()) as h:
+        Yd = torch.from_numpy(Y).cuda()
+        h.set_algorithm("projection")
+        with pytest.raises(OmpError) as ei:
+            h.batch(Yd, S)
+        assert ei.value.status == 6
+        h.set_algorithm("auto")
+        r = h.batch(Yd, S)
+        torch.cuda.synchronize()
+        assert h.last_path() == "residual"
+        out = dict(support=r.support.cpu().numpy(), X=r.X.cpu().numpy(), resid=r.resid_norm.cpu().numpy(),
+                   n_iter=r.n_iter.cpu().numpy(), status=r.status.cpu().numpy())
+    assert_no_bugs(parity(out, A, Y, S, None, range(4)), "N=9000 residual")
