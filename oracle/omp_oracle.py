@@ -36,7 +36,8 @@ Besides the result, every step records the diagnostics the parity protocol
 needs: the top-two normalised correlations, the primary and
 extended near-tie flags, the eps stop margin and the pivot ratio.
 
-Pinned by tests/test_oracle_pins.py (P1-P10); see DESIGN.md §4.
+Pinned by tests/test_oracle_pins.py (P1-P11; P11 pins the per-step diagnostics and
+first_flag() the parity protocol relies on); see DESIGN.md §4.
 """
 
 from __future__ import annotations
@@ -237,8 +238,9 @@ def omp_batch(A, Y, S: int, eps: Optional[float] = None, workers: Optional[int] 
         chunk = max(1, -(-B // (workers * 4)))
     parts = [Y[i:i + chunk] for i in range(0, B, chunk)]
     ctx = mp.get_context("fork")
+    # the workers get A exactly as given (promoted to FP64 by _worker_init, like the serial path)
     with ProcessPoolExecutor(max_workers=workers, mp_context=ctx, initializer=_worker_init,
-                             initargs=(np.asarray(A, np.float32), S, eps)) as ex:
+                             initargs=(np.asarray(A), S, eps)) as ex:
         out: List[OracleResult] = []
         for part in ex.map(_worker_run, parts):
             out.extend(part)

@@ -53,8 +53,18 @@ def parity(out, A_np, Y_np, S, eps, rows, workers=None):
                          A_np.shape[1], rows=rows)
 
 
-def assert_no_bugs(rep, label=""):
+# Excused outcomes ("tie_divergent": after a primary/stop/near-degenerate flag; "explained": at a step
+# only the extended rule flags) are bounded: the oracle flags ~0-3 % of signals on the configs
+# (SURVEY §8(c) numerical study: c4 3.0 %, c3 0.5-0.7 %, c2 0.1 %, tiny / c5 0 %), and most flagged
+# signals still agree ("flagged_ok").  A systematic selection error near ties would exceed this.
+EXCUSED_FRAC = 0.05
+
+
+def assert_no_bugs(rep, label="", max_excused_frac=EXCUSED_FRAC):
     d = rep.as_dict()
     print(f"parity {label}: {d}")
     assert rep.counts.get("bug", 0) == 0, d
+    n = sum(rep.counts.values())
+    excused = rep.counts.get("tie_divergent", 0) + rep.counts.get("explained", 0)
+    assert excused <= int(max_excused_frac * n) + 1, (f"{excused} excused of {n}", d)
     return d

@@ -323,3 +323,117 @@ def test_c3_noise_eps_stops_sample():
         assert r.status == EPS and r.resid_norm <= prob.eps
         assert all(s.resid_norm > prob.eps for s in r.steps[:-1])
         assert 8 <= r.n_iter <= prob.S
+
+
+def test_p8_worker_path_keeps_fp64_inputs():
+    """The worker pool gets A exactly as given: an FP64 dictionary (not representable in FP32) gives
+    bit-identical results on the serial and the parallel path."""
+    A = _gauss(24, 48, 51)                  # FP64, unit columns
+    rng = np.random.default_rng(52)
+    Y = np.stack([A[:, rng.choice(48, 3, replace=False)] @ rng.standard_normal(3) for _ in range(6)])
+    serial = omp_batch(A, Y, 5, workers=1)
+    par = omp_batch(A, Y, 5, workers=3, chunk=2)
+    for a, b in zip(serial, par):
+        assert list(a.support) == list(b.support) and np.array_equal(a.x, b.x)
+        assert a.resid_norm == b.resid_norm
+
+
+# ---------------------------------------------------------------- P11: per-step diagnostics
+# The parity protocol (tests/parity.py) excuses a divergence only at a step the oracle flags, so the
+# flags are pinned here on constructed cases whose gaps, margins and pivots are known in closed form
+# (SURVEY §8(c) ambiguities 6, 8, 9; BASELINE.json north_star "top-two within 1e-5 relative").
+def _two_atoms_gap(g, z=0.0):
+    """A = [e1, e2] in R^3, y = (1, 1 - g, z): t1 = 1 (atom 0), t2 = 1 - g, ||y|| = sqrt(1 + (1-g)^2 + z^2)."""
+    A = np.eye(3)[:, :2]
+    return A, np.array([1.0, 1.0 - g, z])
+
+
+def test_p11_primary_tie_threshold():
+    A, y = np.eye(3), np.array([1.0, 1.0, 0.0])            # exact tie
+    r = omp(A, y, 2)
+    st = r.steps[0]
+    assert (st.t1, st.t2) == (1.0, 1.0) and st.primary_tie and st.extended_tie
+    assert r.first_flag() == 0 and r.first_flag(extended=True) == 0
+    for g, want in ((0.5e-5, True), (0.99e-5, True), (1.01e-5, False), (2e-5, False)):
+        A, y = _two_atoms_gap(g)
+        st = omp(A, y, 1).steps[0]
+        assert st.t1 == 1.0 and st.t2 == pytest.approx(1.0 - g, abs=1e-15)
+        assert st.primary_tie == want, g
+        assert omp(A, y, 1).first_flag() == (0 if want else None)
+
+
+def test_p11_extended_tie_adds_2e_6_ynorm():
+    # ||y|| ~ 10: extended threshold 1e-5 t1 + 2e-6 ||y|| ~ 3.0e-5, primary 1e-5
+    for g, primary, extended in ((0.5e-5, True, True), (2e-5, False, True), (2.9e-5, False, True),
+                                 (3.2e-5, False, False), (5e-5, False, False)):
+        A, y = _two_atoms_gap(g, z=10.0)
+        r = omp(A, y, 1)
+        st = r.steps[0]
+        yn = float(np.linalg.norm(y))
+        assert 1e-5 + 2e-6 * yn == pytest.approx(3.02e-5, abs=1e-7)
+        assert (st.primary_tie, st.extended_tie) == (primary, extended), g
+        assert r.first_flag() == (0 if primary else None)
+        assert r.first_flag(extended=True) == (0 if extended else None)
+
+
+def test_p11_stop_flag_and_init_stop_flag():
+    A = np.eye(3)[:, :2]
+    y = np.array([3.0, 0.0, 4.0])                           # after step 1: r = (0, 0, 4), ||r|| = 4
+    for eps, flag, status, k in ((4 * (1 + 5e-6), True, EPS, 1), (4 * (1 - 5e-6), True, MAXITER, 1),
+                                 (4 * (1 + 5e-5), False, EPS, 1), (4 * (1 - 5e-5), False, MAXITER, 1)):
+        r = omp(A, y, 1, eps=eps)
+        assert r.steps[0].resid_norm == 4.0
+        assert r.steps[0].stop_flag == flag and r.status == status and r.n_iter == k, eps
+        assert not r.init_stop_flag
+        assert r.first_flag() == (0 if flag else None)
+    # the k = 0 test on ||y|| = 5 (reading R2)
+    # (eps < ||y|| = 5 goes on to step 1, whose ||r|| = 4 <= eps stops it)
+    for eps, flag, k in ((5 * (1 + 5e-6), True, 0), (5 * (1 - 5e-6), True, 1),
+                         (5 * (1 + 5e-5), False, 0), (5 * (1 - 5e-5), False, 1)):
+        r = omp(A, y, 1, eps=eps)
+        assert r.init_stop_flag == flag, eps
+        assert r.status == EPS and r.n_iter == k
+        if flag:
+            assert r.first_flag() == 0 and r.first_flag(extended=True) == 0
+    assert omp(A, y, 1).init_stop_flag is False             # no eps: never flagged
+
+
+def test_p11_near_degenerate_pivot():
+    """a0 = e1, a1 = (cos t, sin t), y = (1, 1): step 1 takes a1 (correlation cos t + sin t > 1), step 2
+    a0, whose QR pivot after a1 has R_22^2 / ||a0||^2 = sin^2 t; flagged below 1e-4."""
+    for s2, flag in ((5e-5, True), (0.99e-4, True), (1.01e-4, False), (2e-4, False)):
+        t = np.arcsin(np.sqrt(s2))
+        A = np.array([[1.0, np.cos(t)], [0.0, np.sin(t)]])
+        y = np.array([1.0, 1.0])
+        r = omp(A, y, 2)
+        assert r.n_iter == 2
+        st = r.steps[1]
+        assert st.pivot_ratio == pytest.approx(s2, rel=1e-9)
+        assert st.near_degenerate == flag and not r.steps[0].near_degenerate
+        assert not r.steps[0].primary_tie and not r.steps[1].primary_tie   # gaps ~ sin t >= 7e-3
+        assert r.first_flag() == (1 if flag else None)
+
+
+def test_p11_first_flag_is_the_first_flagged_step():
+    """Orthonormal A, |A^T y| = (4, 3, 2, 2, 1): steps 1-2 clear (gaps 1), step 3 an exact tie."""
+    A = np.eye(5)
+    y = np.array([4.0, 3.0, 2.0, 2.0, 1.0])
+    r = omp(A, y, 4)
+    assert [s.primary_tie for s in r.steps] == [False, False, True, False]
+    assert r.first_flag() == 2 and r.first_flag(extended=True) == 2
+    # a step flagged only by the extended rule comes first: ||y|| large against the gap at step 1
+    y = np.array([1.0, 1.0 - 2e-5, 0.5, 0.5, 0.0])
+    A = np.eye(6)[:, :5]
+    y6 = np.r_[y, 10.0]
+    r = omp(A, y6, 4)
+    assert r.steps[0].extended_tie and not r.steps[0].primary_tie
+    assert r.first_flag(extended=True) == 0
+    assert r.first_flag() == 2                            # the exact tie 0.5 / 0.5 at step 3
+
+
+def test_p11_degenerate_steps_are_flagged():
+    """An exhausted residual (max correlation 0) and a re-selection stop DEGENERATE on a flagged step."""
+    r = omp(np.eye(2), np.array([1.0, 0.0]), 2)
+    assert r.status == DEGENERATE and r.n_iter == 1
+    assert r.steps[1].t1 == 0.0 and r.steps[1].near_degenerate
+    assert r.first_flag() == 1
