@@ -230,6 +230,9 @@ def main():
     dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     if world > 1:
+        # NCCL's init log on stderr shows the ranks and the transports it picked (NVLink / NVLS)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -240,33 +243,14 @@ def main():
     lo, hi = rank * per, min(B_total, (rank + 1) * per)
     B = max(0, hi - lo)
     M, N, S, eps = cfg["M"], cfg["N"], cfg["S"], cfg["eps"]
-
-    # dictionary: generated on rank 0, broadcast once over NCCL (north star); signals: own shard
-    A_np = make_dictionary(M, N, cfg["seed"])
-    comm = dev if args.dist_backend == "nccl" else torch.device("cpu")
-    A = torch.from_numpy(A_np).to(comm) if rank == 0 else torch.empty((M, N), dtype=torch.float32, device=comm)
-    if world > 1:
-        dist.broadcast(A, src=0)          # once per dictionary, over NVLink with NCCL
-    A = A.to(dev)
-    Y_np = make_signals(A.cpu().numpy(), range(lo, hi), cfg["seed"], cfg["sparsity"], cfg["sigma"], device=dev)
-    Y = torch.from_numpy(Y_np).to(dev)
     eps32 = None if eps is None else float(np.float32(eps))
-
-    # ompCreate (validation, norms, screen planes, Gram G = A^T A) timed on its own
-    torch.cuda.synchronize()
-    t_setup = time.perf_counter()
-    h = OMP(A, mode=args.mode)
-    torch.cuda.synchronize()
-    setup_ms = (time.perf_counter() - t_setup) * 1e3
-    if args.small_limit != -1:
-        h.set_small_batch_limit(args.small_limit)
-    if args.algo != "auto":
-        h.set_algorithm(args.algo)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    comm = dev if args.dist_backend == "nccl" else torch.device("cpu")
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
@@ -275,12 +259,48 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # inputs: A and the whole batch on rank 0 (device-resident); with N > 1 the library's distributed
+    # driver broadcasts A once and, every step, scatters Y's slices from rank 0 and gathers the results
+    # back to it (the timed span runs from the scatter to the gather)
+    A_np = make_dictionary(M, N, cfg["seed"])
+    Y_np = None
+    if rank == 0:
+        Y_np = make_signals(A_np, range(B_total), cfg["seed"], cfg["sparsity"], cfg["sigma"], device=dev)
+    Y = torch.from_numpy(Y_np).to(dev) if rank == 0 else None
+
+    # ompCreate (validation, norms, screen planes, Gram G = A^T A) timed on its own;
+    # with N > 1 this includes the broadcast of A over NCCL (max over ranks)
+    barrier()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
+    if world > 1:
+        from paper_2407_06434_b200.distributed import DistributedOMP
+        dist_omp = DistributedOMP(torch.from_numpy(A_np).to(dev) if rank == 0 else None, mode=args.mode,
+                                  device=dev)
+        h = dist_omp.handle
+        A = dist_omp.A.to(dev)
+        solve = lambda: dist_omp.batch(Y, S, eps32)          # noqa: E731  (None on ranks != 0)
+    else:
+        dist_omp = None
+        A = torch.from_numpy(A_np).to(dev)
+        h = OMP(A, mode=args.mode)
+        solve = lambda: h.batch(Y, S, eps32)                 # noqa: E731
+    torch.cuda.synchronize()
+    setup_ms = max_over_ranks((time.perf_counter() - t_setup) * 1e3)
+    if args.small_limit != -1:
+        h.set_small_batch_limit(args.small_limit)
+    if args.algo != "auto":
+        h.set_algorithm(args.algo)
+
     # warm-up (untimed)
     for _ in range(args.warmup):
-        res = h.batch(Y, S, eps32)
+        res = solve()
     torch.cuda.synchronize()
+    barrier()
 
-    # timed region: per-kernel CUDA events inside the library (profiling mode) + step events
+    # timed region: the graph path the library runs by default; with kernel profiling (default) the
+    # captured graph carries an event-record node at every kernel boundary, so each kernel's time is
+    # measured live inside the timed steps, on the library's launch stream
     h.profile(not args.no_kernel_profile)
     h.profile_read(reset=True)
     props = torch.cuda.get_device_properties(dev)
@@ -289,7 +309,8 @@ def main():
     step_ms = []
     launches = 0
     # inputs smaller than 2x L2 (126 MB): flush L2 between timed steps by writing 256 MB
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if Y_np.nbytes < (252 << 20) else None
+    y_bytes = B * M * 4
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if y_bytes < (252 << 20) else None
     for _ in range(args.steps):
         if flush is not None:
             flush.zero_()
@@ -298,34 +319,52 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = h.batch(Y, S, eps32)
+        res = solve()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
         launches += h.launch_count()
-        h.profile_read(reset=False)      # per-kernel event pairs of this step (graph replays reuse them)
+        h.profile_read(reset=False)      # per-kernel event pairs of this step
     clk = clocks.stop()
     kern = h.profile_read(reset=True)
     if args.no_kernel_profile:           # kernel split from one extra, profiled step
         h.profile(True)
-        h.batch(Y, S, eps32)
+        solve()
         torch.cuda.synchronize()
         kern = h.profile_read(reset=True)
     h.profile(False)
     ms = statistics.mean(step_ms)
     value = B_total / (ms / 1e3)
+    if world > 1:
+        # every rank's own launches; the line reports the sum over ranks
+        t = torch.tensor([launches], dtype=torch.float64, device=comm)
+        dist.all_reduce(t)
+        launches = int(t.item())
 
-    # end to end through the public host API: pinned host Y in, host results out, every step
+    # end to end through the public API: pinned host Y in, host results out, every step.  N = 1:
+    # ompBatchHost (copies inside the library call); N > 1: the distributed driver on rank 0's pinned
+    # host batch (H2D to rank 0, scatter, solve, gather, D2H of the gathered results)
     e2e = None
     if not args.no_e2e and B > 0:
-        Yh = torch.from_numpy(Y_np).pin_memory()
-        outs = (torch.empty((B, S), dtype=torch.float32).pin_memory().numpy(),
-                torch.empty((B, S), dtype=torch.int32).pin_memory().numpy(),
-                torch.empty((B,), dtype=torch.float32).pin_memory().numpy(),
-                torch.empty((B,), dtype=torch.int32).pin_memory().numpy(),
-                torch.empty((B,), dtype=torch.int32).pin_memory().numpy())
-        h.batch_host(Yh.numpy(), S, eps32, out=outs)   # warm the staging buffers
+        outs = (torch.empty((B_total, S), dtype=torch.float32).pin_memory(),
+                torch.empty((B_total, S), dtype=torch.int32).pin_memory(),
+                torch.empty((B_total,), dtype=torch.float32).pin_memory(),
+                torch.empty((B_total,), dtype=torch.int32).pin_memory(),
+                torch.empty((B_total,), dtype=torch.int32).pin_memory()) if rank == 0 else None
+        Yh = torch.from_numpy(Y_np).pin_memory() if rank == 0 else None
+
+        def e2e_step():
+            if world == 1:
+                h.batch_host(Yh.numpy(), S, eps32, out=tuple(o.numpy() for o in outs))
+                return
+            r = dist_omp.batch(Yh.to(dev, non_blocking=True) if rank == 0 else None, S, eps32)
+            if rank == 0:
+                for o, f in zip(outs, ("X", "support", "resid_norm", "n_iter", "status")):
+                    o.copy_(getattr(r, f), non_blocking=True)
+
+        e2e_step()                       # warm the staging buffers
+        torch.cuda.synchronize()
         e2e_ms = []
         for _ in range(args.e2e_steps):
             barrier()
@@ -333,18 +372,26 @@ def main():
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-            h.batch_host(Yh.numpy(), S, eps32, out=outs)
+            e2e_step()
             t1.record(stream)
             torch.cuda.synchronize()
             barrier()
             e2e_ms.append(max_over_ranks(t0.elapsed_time(t1)))
         e2e = {"value": B_total / (statistics.mean(e2e_ms) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(Y_np.nbytes) * world,
-               "d2h_bytes_per_step": int(sum(o.nbytes for o in outs)) * world}
+               "h2d_bytes_per_step": int(B_total * M * 4),
+               "d2h_bytes_per_step": int(B_total * (8 * S + 12))}
 
     # roofline of the dominant kernel (events measured live over the timed steps, this rank)
     path = h.last_path()
-    work = kernel_work(cfg, B, args.mode, path, res.n_iter.cpu().numpy() if B > 0 else None)
+    n_iter_here = None
+    if B > 0:
+        if world == 1:
+            n_iter_here = res.n_iter.cpu().numpy()
+        else:
+            # this rank's slice of the gathered result is on rank 0 only: count its iterations from its
+            # own per-launch live counts instead (every rank runs the same S launches)
+            n_iter_here = rank_n_iter(dist_omp, res, rank, world, B_total, comm)
+    work = kernel_work(cfg, B, args.mode, path, n_iter_here)
     dom = max((k for k in kern if k in work), key=lambda k: kern[k][0])
     bound, per_launch, unit, split = work[dom]
     peak_mode = args.mode
@@ -408,6 +455,9 @@ def main():
     parity_rep = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, parity_rep = cpu_baseline(args, cfg, A_np, Y_np, res, lo)
+    elif rank == 0 and world > 1 and not args.no_cpu_baseline:
+        # parity of the gathered multi-GPU result on the shard boundaries (no oracle timing at N > 1)
+        parity_rep = shard_parity(cfg, A_np, Y_np, res, world)
 
     if rank == 0:
         line = {
@@ -420,9 +470,12 @@ def main():
                        "M": M, "N": N, "S": S, "global_batch": B_total, "per_gpu_batch": per,
                        "mode": args.mode, "screen_dtype": {"bf16": "bf16", "3xtf32": "tf32x3", "simt": "none"}[args.mode],
                        "l2": ("L2 flushed between timed steps (256 MB write; Y %.1f MB/rank)" if flush is not None
-                              else "inputs larger than L2 (Y %.0f MB/rank)") % (Y_np.nbytes / 1e6),
+                              else "inputs larger than L2 (Y %.0f MB/rank)") % (y_bytes / 1e6),
                        "path": path,
-                       "parallelism": f"batch-shard x{world}"},
+                       "parallelism": f"batch-shard x{world}",
+                       "collectives": ("none" if world == 1 else
+                                       "NCCL: A broadcast once (setup); per step scatter Y from rank 0, "
+                                       "gather the packed results to rank 0 (inside the timed span)")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "kernels": kernels,
             "setup_ms": setup_ms,
@@ -430,9 +483,49 @@ def main():
         if parity_rep is not None:
             line["parity"] = parity_rep
         print(json.dumps(line), flush=True)
-    h.close()
+    if dist_omp is not None:
+        dist_omp.close()
+    else:
+        h.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def rank_n_iter(dist_omp, res, rank, world, B_total, comm):
+    """Iterations each signal of this rank's slice ran: rank 0 has the gathered result and scatters
+    the slices' n_iter back (outside the timed region)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2407_06434_b200.distributed import shard_bounds
+    per = -(-B_total // world)
+    mine = torch.zeros(per, dtype=torch.int32, device=comm)
+    chunks = None
+    if rank == 0:
+        ni = res.n_iter.to(comm)
+        chunks = []
+        for r in range(world):
+            a, b, _ = shard_bounds(B_total, world, r)
+            c = torch.zeros(per, dtype=torch.int32, device=comm)
+            c[: b - a] = ni[a:b]
+            chunks.append(c)
+    dist.scatter(mine, chunks, src=0)
+    lo, hi, _ = shard_bounds(B_total, world, rank)
+    return mine[: hi - lo].cpu().numpy()
+
+
+def shard_parity(cfg, A_np, Y_np, res, world):
+    """Oracle parity of the gathered result at the ends of every rank's slice (8 signals each)."""
+    from oracle import host_cores, omp_batch as oracle_batch
+    from paper_2407_06434_b200.distributed import shard_bounds
+    from parity import compare_batch
+    B = len(Y_np)
+    rows = sorted({b for r in range(world) for (lo, hi, _) in [shard_bounds(B, world, r)]
+                   for b in list(range(lo, min(hi, lo + 4))) + list(range(max(lo, hi - 4), hi))})
+    eps32 = None if cfg["eps"] is None else float(np.float32(cfg["eps"]))
+    ora = oracle_batch(A_np, Y_np[rows], cfg["S"], eps32, workers=host_cores())
+    rep = compare_batch(res.support.cpu().numpy(), res.X.cpu().numpy(), res.resid_norm.cpu().numpy(),
+                        res.n_iter.cpu().numpy(), res.status.cpu().numpy(), ora, A_np.shape[1], rows=rows)
+    return rep.as_dict()
 
 
 def oracle_sample_size(args, cfg, cores):

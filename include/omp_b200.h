@@ -144,7 +144,15 @@ ompStatus_t ompGetGram(ompHandle_t handle, float* G, int64_t ldg, void* stream);
 ompStatus_t ompGetFactor(ompHandle_t handle, int64_t b0, int64_t count, float* F, float* u,
                          void* stream);
 
-/* Profiling: when enabled, ompBatch brackets every kernel with CUDA events on `stream`;
+/* ompSetGraphs — a batch's launch sequence (1 + 2S kernels; 1 + 3S in SIMT mode) is captured into a
+ *   CUDA graph on first use and replayed on later calls with the same shape, eps and buffers
+ *   (enable = 1, default; one graph launch per batch, PAPER.md:243 on per-call
+ *   overhead), or launched kernel by kernel (enable = 0; debugging, sanitizers).  Same results.   */
+ompStatus_t ompSetGraphs(ompHandle_t handle, int enable);
+
+/* Profiling: when enabled, ompBatch brackets every kernel with CUDA events on `stream` (in the
+ * captured graph: an external event-record node on either side of every kernel node, so a replayed
+ * batch times its own kernels; a replay collects an earlier unread replay's times first);
  * ompProfileRead returns, per kernel slot (0 init, 1 correlation, 2 standalone argmax [SIMT
  * mode], 3 update = exact selection + factor append + residual, 4 small-batch persistent
  * kernel = all S iterations of a small batch in one launch), the summed
@@ -184,16 +192,21 @@ ompStatus_t ompSetSmallBatchLimit(ompHandle_t handle, int64_t max_batch);
 typedef enum { OMP_PATH_RESIDUAL = 0, OMP_PATH_SMALL = 1, OMP_PATH_PROJECTION = 2 } ompPath_t;
 int ompGetLastPath(ompHandle_t handle);
 
-/* Kernel launches issued by the last ompBatch (for launch accounting).                   */
+/* Kernel launches issued by the last ompBatch (launch accounting; the per-iteration kernel
+ * sequence of SURVEY §8(a) a1-a5: 1 + 2S, 1 + 3S in SIMT mode, 2 on the small-batch path).  */
 int64_t ompGetLaunchCount(ompHandle_t handle);
 
-/* Release everything the handle owns (synchronises its device).                          */
+/* ompDestroy — release everything the handle owns (synchronises its device): the dictionary
+ *   copies and Gram matrix of ompCreate, the batch workspaces, cached graphs; restores the device's
+ *   persisting-L2 limit when the last handle on the device goes (ownership: SURVEY §8(b)).     */
 ompStatus_t ompDestroy(ompHandle_t handle);
 
+/* ompGetErrorString — static text of a call-level status (SURVEY §8(b) "Errors").          */
 const char* ompGetErrorString(ompStatus_t status);
 
-/* Detail of the last error on this handle (offending column, cudaError_t, ...);
- * with handle == NULL, the detail of the last failed ompCreate on this thread.           */
+/* ompGetErrorDetail — detail of the last error on this handle (the offending column of a zero or
+ * non-finite atom, S:117-120 / S:132; a cudaError_t, ...); with handle == NULL, the detail of the
+ * last failed ompCreate on this thread.                                                   */
 int64_t ompGetErrorDetail(ompHandle_t handle);
 
 /* omp_batch — one-shot convenience in the north-star's phrasing

@@ -52,6 +52,7 @@ SIGNATURES = {
     "ompScreeningWindow": (c_float, [c_int, c_int64]),
     "ompGetGram": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "ompGetFactor": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ompSetGraphs": (c_int, [c_void_p, c_int]),
     "ompProfileEnable": (c_int, [c_void_p, c_int]),
     "ompProfileRead": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), c_int]),
     "ompGetLaunchCount": (c_int64, [c_void_p]),

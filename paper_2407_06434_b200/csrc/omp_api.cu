@@ -28,6 +28,7 @@ using namespace ompb;
 struct ProfRec {
   int slot;
   cudaEvent_t a, b;
+  bool graph_owned;   // recorded by an event node of a cached CUDA graph (destroyed with the graph)
 };
 
 // everything a captured batch bakes in
@@ -36,8 +37,9 @@ struct GraphKey {
   int32_t S;
   float eps;
   const void *Y, *X, *support, *resid, *n_iter, *status;
+  bool prof;          // captured with an event-record node around every kernel (profiling mode)
   bool operator==(const GraphKey& o) const {
-    return B == o.B && ldy == o.ldy && ldx == o.ldx && lds == o.lds && S == o.S &&
+    return B == o.B && ldy == o.ldy && ldx == o.ldx && lds == o.lds && S == o.S && prof == o.prof &&
            (eps == o.eps || (eps != eps && o.eps != o.eps)) && Y == o.Y && X == o.X && support == o.support &&
            resid == o.resid && n_iter == o.n_iter && status == o.status;
   }
@@ -97,6 +99,7 @@ struct ompHandle_st {
   bool profile = false;
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> ev_pool;
+  std::vector<ProfRec>* prof_capture = nullptr;   // while capturing a profiled graph: its event pairs
   // CUDA graphs of recent batches' launch sequences (small LRU: callers that alternate output
   // buffers, e.g. a fresh allocation per call under the caching allocator, still hit)
   cudaStream_t cap_stream = nullptr;
@@ -106,11 +109,13 @@ struct ompHandle_st {
     int64_t launches = 0;
     int path = 0;
     uint64_t used = 0;
+    std::vector<ProfRec> prof;   // profiled graphs: the (slot, start, end) event nodes, in launch order
   };
   static constexpr int kGraphCache = 4;
   GraphEntry graphs[kGraphCache];
   uint64_t graph_tick = 0;
   bool graph_broken = false;
+  bool use_graphs = true;     // ompSetGraphs
   double prof_ms[OMP_NUM_KERNEL_SLOTS] = {0};
   int64_t prof_n[OMP_NUM_KERNEL_SLOTS] = {0};
 };
@@ -164,11 +169,24 @@ static void dfree(T*& p) {
   p = nullptr;
 }
 
+// OMP_B200_DEBUG_FILL=1: every buffer the library allocates starts as 0xFF bytes (NaN floats, -1
+// ints), so a kernel that reads workspace it never wrote shows up as NaN / garbage results in the
+// parity tests (run by scripts/sanitize.sh next to compute-sanitizer initcheck)
+static bool debug_fill() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OMP_B200_DEBUG_FILL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <typename T>
 static bool dalloc(T*& p, size_t count) {
   dfree(p);
   if (count == 0) count = 1;
-  return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)) == cudaSuccess;
+  if (cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)) != cudaSuccess) return false;
+  return !debug_fill() || cudaMemset(p, 0xFF, count * sizeof(T)) == cudaSuccess;
 }
 
 static ompStatus_t cuda_fail(ompHandle_t h, cudaError_t e) {
@@ -226,33 +244,75 @@ static float screening_window(int mode, int64_t Kp) {
   return (float)(2.0 * (c0 + c_refine) * 1.25);
 }
 
+// Profiling mode brackets every kernel with a pair of CUDA events on its launch stream: recorded
+// directly, or -- while a batch is being captured into a CUDA graph -- as external event-record nodes
+// of the graph (cudaEventRecordExternal), so the replayed graph times each kernel itself.
 struct Launcher {
   ompHandle_t h;
   cudaStream_t st;
   int64_t count = 0;
   cudaEvent_t a = nullptr;
+  void record(cudaEvent_t e) {
+    if (h->prof_capture) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+  }
   void begin(int slot) {
     (void)slot;
     if (h->profile) {
       a = take_event(h);
-      cudaEventRecord(a, st);
+      record(a);
     }
   }
   void end(int slot) {
     ++count;
     if (h->profile) {
       cudaEvent_t b = take_event(h);
-      cudaEventRecord(b, st);
-      h->prof_pending.push_back({slot, a, b});
+      record(b);
+      if (h->prof_capture) h->prof_capture->push_back({slot, a, b, true});
+      else h->prof_pending.push_back({slot, a, b, false});
     }
   }
 };
 
-static void invalidate_graph(ompHandle_t h) {
-  for (auto& g : h->graphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g = ompHandle_st::GraphEntry{};
+// fold the pending event pairs into the per-slot sums (synchronises their events)
+static cudaError_t profile_collect(ompHandle_t h) {
+  for (auto& r : h->prof_pending) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) return e;
+    h->prof_ms[r.slot] += t;
+    h->prof_n[r.slot] += 1;
+    if (!r.graph_owned) {
+      h->ev_pool.push_back(r.a);
+      h->ev_pool.push_back(r.b);
+    }
   }
+  h->prof_pending.clear();
+  return cudaSuccess;
+}
+
+static void destroy_entry(ompHandle_t h, ompHandle_st::GraphEntry& g) {
+  if (!g.prof.empty()) {
+    // an unread replay of this graph: its times are dropped with its events
+    std::vector<ProfRec> keep;
+    for (auto& r : h->prof_pending) {
+      bool mine = false;
+      for (auto& q : g.prof) mine |= (q.a == r.a);
+      if (!mine) keep.push_back(r);
+    }
+    h->prof_pending.swap(keep);
+    for (auto& q : g.prof) {
+      cudaEventDestroy(q.a);
+      cudaEventDestroy(q.b);
+    }
+  }
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g = ompHandle_st::GraphEntry{};
+}
+
+static void invalidate_graph(ompHandle_t h) {
+  for (auto& g : h->graphs) destroy_entry(h, g);
 }
 
 static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
@@ -606,10 +666,9 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     const char* e = getenv("OMP_B200_GRAPH");
     env_graph = (e && e[0] == '0') ? 0 : 1;
   }
-  // profiling brackets every kernel with events: launch directly (event nodes in a graph cost more)
-  if (h->profile || !env_graph || h->graph_broken)
+  if (!env_graph || !h->use_graphs || h->graph_broken)
     return enqueue_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, st);
-  const GraphKey key{B, ldy, ldx, lds, S, eps, Y, X, support, resid, n_iter, status};
+  const GraphKey key{B, ldy, ldx, lds, S, eps, Y, X, support, resid, n_iter, status, h->profile};
   ompHandle_st::GraphEntry* hit = nullptr;
   for (auto& g : h->graphs)
     if (g.exec && g.key == key) hit = &g;
@@ -617,20 +676,26 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     hit = &h->graphs[0];                    // evict an empty or the least recently used entry
     for (auto& g : h->graphs)
       if (!g.exec || g.used < hit->used) hit = &g;
-    if (hit->exec) cudaGraphExecDestroy(hit->exec);
-    *hit = ompHandle_st::GraphEntry{};
+    destroy_entry(h, *hit);
     if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
       return cuda_fail(h, cudaGetLastError());
     // capture only records the launches; the replay is ordered on the caller's stream
     cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_fail(h, e);
+    std::vector<ProfRec> prof;
+    if (h->profile) h->prof_capture = &prof;
     s = enqueue_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status, h->cap_stream);
+    h->prof_capture = nullptr;
     cudaGraph_t g = nullptr;
     e = cudaStreamEndCapture(h->cap_stream, &g);
     if (s == OMP_OK && e == cudaSuccess) e = cudaGraphInstantiate(&hit->exec, g, 0);
     if (g) cudaGraphDestroy(g);
     if (s != OMP_OK || e != cudaSuccess) {
       cudaGetLastError();
+      for (auto& q : prof) {
+        cudaEventDestroy(q.a);
+        cudaEventDestroy(q.b);
+      }
       hit->exec = nullptr;
       h->graph_broken = true;               // never try again on this handle; launch directly
       if (s != OMP_OK && s != OMP_ERR_CUDA) return s;
@@ -639,10 +704,21 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     hit->key = key;
     hit->launches = h->last_launches;
     hit->path = h->last_path;
+    hit->prof.swap(prof);
+  }
+  if (!hit->prof.empty()) {
+    // the graph re-records the same events: collect an unread earlier replay's times first
+    bool pending = false;
+    for (auto& r : h->prof_pending) pending |= r.graph_owned && r.a == hit->prof.front().a;
+    if (pending) {
+      cudaError_t e = profile_collect(h);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    }
   }
   hit->used = ++h->graph_tick;
   cudaError_t e = cudaGraphLaunch(hit->exec, st);
   if (e != cudaSuccess) return cuda_fail(h, e);
+  for (auto& q : hit->prof) h->prof_pending.push_back(q);
   h->last_launches = hit->launches;
   h->last_path = hit->path;
   h->lastB = B;
@@ -986,6 +1062,12 @@ ompStatus_t ompGetFactor(ompHandle_t h, int64_t b0, int64_t count, float* F, flo
   return e == cudaSuccess ? OMP_OK : cuda_fail(h, e);
 }
 
+ompStatus_t ompSetGraphs(ompHandle_t h, int enable) {
+  if (!h) return OMP_ERR_INVALID_ARG;
+  h->use_graphs = enable != 0;
+  return OMP_OK;
+}
+
 ompStatus_t ompProfileEnable(ompHandle_t h, int enable) {
   if (!h) return OMP_ERR_INVALID_ARG;
   h->profile = enable != 0;
@@ -995,17 +1077,8 @@ ompStatus_t ompProfileEnable(ompHandle_t h, int enable) {
 ompStatus_t ompProfileRead(ompHandle_t h, double* ms, int64_t* launches, int reset) {
   if (!h) return OMP_ERR_INVALID_ARG;
   DevGuard g(h->device);
-  for (auto& r : h->prof_pending) {
-    float t = 0.f;
-    cudaError_t e = cudaEventSynchronize(r.b);
-    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
-    if (e != cudaSuccess) return cuda_fail(h, e);
-    h->prof_ms[r.slot] += t;
-    h->prof_n[r.slot] += 1;
-    h->ev_pool.push_back(r.a);
-    h->ev_pool.push_back(r.b);
-  }
-  h->prof_pending.clear();
+  cudaError_t e = profile_collect(h);
+  if (e != cudaSuccess) return cuda_fail(h, e);
   for (int i = 0; i < OMP_NUM_KERNEL_SLOTS; ++i) {
     if (ms) ms[i] = h->prof_ms[i];
     if (launches) launches[i] = h->prof_n[i];

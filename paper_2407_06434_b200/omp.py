@@ -159,6 +159,10 @@ class OMP:
                                   Xd.stride(0), _stream_ptr(stream, self.device)), "ompDensify", self.handle)
         return Xd
 
+    def set_graphs(self, enable: bool = True):
+        """Capture batches into CUDA graphs and replay them (default) or launch kernel by kernel."""
+        check(self.lib.ompSetGraphs(self.handle, int(enable)), "ompSetGraphs", self.handle)
+
     def profile(self, enable: bool = True):
         check(self.lib.ompProfileEnable(self.handle, int(enable)), "ompProfileEnable", self.handle)
 

@@ -60,6 +60,16 @@ def parity(out, A_np, Y_np, S, eps, rows, workers=None):
 EXCUSED_FRAC = 0.05
 
 
+def parity_cached(out, prob, rows, cache_name, workers=None):
+    """parity() on rows of a synth Problem, the oracle taken from tests/golden/oracle_cache when the
+    signal's FP32 bytes match the cached input (else computed now)."""
+    from oracle_cache import oracle_for_rows
+    rows = [int(r) for r in rows]
+    ora, _ = oracle_for_rows(cache_name, prob.A, prob.Y, rows, prob.indices, prob.S, eps32(prob.eps), workers)
+    return compare_batch(out["support"], out["X"], out["resid"], out["n_iter"], out["status"], ora,
+                         prob.A.shape[1], rows=rows)
+
+
 def assert_no_bugs(rep, label="", max_excused_frac=EXCUSED_FRAC):
     d = rep.as_dict()
     print(f"parity {label}: {d}")

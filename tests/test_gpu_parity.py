@@ -11,7 +11,8 @@ import os
 import numpy as np
 import pytest
 
-from gpu_helpers import assert_no_bugs, eps32, parity, run_gpu
+from gpu_helpers import assert_no_bugs, eps32, parity, parity_cached, run_gpu
+from oracle_cache import SAMPLES
 from oracle import DEGENERATE, EPS, MAXITER, NAN
 from synth import make_dictionary, make_problem, make_signals
 
@@ -108,13 +109,20 @@ def test_parity_c2_all(mode):
     assert d["counts"].get("exact", 0) + d["counts"].get("flagged_ok", 0) >= 995
 
 
+@pytest.fixture(scope="module")
+def c3_problem():
+    return make_problem("c3", device="cuda")
+
+
 @pytest.mark.parametrize("mode", LIB_MODES)
-def test_parity_c3_full_batch_sampled(mode):
-    prob = make_problem("c3", device="cuda")
+def test_parity_c3_full_batch_sampled(mode, c3_problem):
+    """c3 at its full batch (B = 10^4, eps stops): 2 000 signals (every 5th) against the oracle
+    (SURVEY §8(d) subsample; cached FP64 results, tests/oracle_cache.py)."""
+    prob = c3_problem
     out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
-    rows = np.unique(np.r_[np.arange(0, 96), np.linspace(0, prob.B - 1, 96).astype(int), prob.B - 1])
-    rep = parity(out, prob.A, prob.Y, prob.S, prob.eps, rows)
-    assert_no_bugs(rep, f"c3/{mode}")
+    rows = SAMPLES["c3"]
+    assert len(rows) == 2000
+    assert_no_bugs(parity_cached(out, prob, rows, "c3"), f"c3/{mode}")
     st = out["status"]
     assert np.mean(st == EPS) > 0.95            # c3 stops by eps (SURVEY §8(d))
 
@@ -127,17 +135,33 @@ def test_parity_c5_sweep_sampled(B):
     assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), f"c5 B={B}")
 
 
-def test_parity_c4_full_batch_sampled():
-    """BASELINE.json's largest config at its full size (B = 1e5), the bench's launch configuration."""
-    prob = make_problem("c4", device="cuda")
-    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "auto")
-    # shard boundaries at 1/2/4/8 GPUs, plus every signal that did not run to S (checked against
-    # the oracle too: an early stop must be the oracle's as well, or a flagged divergence)
+@pytest.fixture(scope="module")
+def c4_problem():
+    return make_problem("c4", device="cuda")
+
+
+@pytest.mark.parametrize("mode", ["auto", "3xtf32"])
+def test_parity_c4_full_batch_sampled(mode, c4_problem):
+    """BASELINE.json's largest config at its full size (B = 1e5), the bench's launch configuration
+    (auto = bf16 screen) and the 3xTF32 screen: the 1 024 signals at the ends of every rank's slice at
+    8 GPUs (cached FP64 results), plus every signal that stopped before S."""
+    prob = c4_problem
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, mode)
     odd = np.flatnonzero((out["status"] != MAXITER) | (out["n_iter"] != prob.S))
-    print(f"c4: {len(odd)} signals stopped before S: statuses {np.unique(out['status'][odd], return_counts=True)}")
+    print(f"c4/{mode}: {len(odd)} signals stopped before S: statuses {np.unique(out['status'][odd], return_counts=True)}")
     assert len(odd) <= 100
-    rows = sorted(set([0, 1, 12499, 12500, 49999, 50000, 87499, 99999]) | set(odd[:16].tolist()))
-    assert_no_bugs(parity(out, prob.A, prob.Y, prob.S, prob.eps, rows), "c4")
+    rows = sorted(set(SAMPLES["c4"].tolist()) | set(odd[:16].tolist()))
+    assert len(rows) >= 1024
+    assert_no_bugs(parity_cached(out, prob, rows, "c4"), f"c4/{mode}")
+
+
+def test_parity_c5_1e6_sampled():
+    """c5 at B = 10^6 (the sweep's largest batch, in the bench's launch configuration): 1 000 signals
+    spread over the batch against cached FP64 results."""
+    prob = make_problem("c5", device="cuda")
+    assert prob.B == 1000000
+    out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "auto")
+    assert_no_bugs(parity_cached(out, prob, SAMPLES["c5"], "c5"), "c5 B=1e6")
 
 
 # ------------------------------------------------------------------ ragged shapes, edge cases
@@ -369,19 +393,19 @@ def _fields(r):
 
 @pytest.mark.parametrize("mode", ["bf16", "simt"])
 def test_graph_replay_matches_direct_launch(mode):
-    """The CUDA-graph replay (default path) equals direct launches (profiling mode) bit for bit,
+    """The CUDA-graph replay (default path) equals direct launches (ompSetGraphs(0)) bit for bit,
     across graph-cache hits, misses (fresh output buffers, new eps, new B) and evictions."""
     import torch
     from paper_2407_06434_b200 import OMP
     prob = make_problem("c2", B=300)
     Y = torch.from_numpy(prob.Y).cuda()
     with OMP(torch.from_numpy(prob.A).cuda(), mode=mode) as h:
-        h.profile(True)
+        h.set_graphs(False)
         want = {}
         for B, eps in [(300, None), (300, 0.3), (77, None)]:
             r = h.batch(Y[:B], prob.S, eps)
             want[(B, eps)] = _fields(r)
-        h.profile(False)
+        h.set_graphs(True)
         for rep in range(3):
             for (B, eps), w in want.items():
                 r = h.batch(Y[:B], prob.S, eps)   # fresh outputs each call
@@ -392,6 +416,21 @@ def test_graph_replay_matches_direct_launch(mode):
         for _ in range(6):                        # > cache size distinct keys: eviction path
             outs = h.batch(Y[:300], prob.S)
         assert np.array_equal(outs.support.cpu().numpy(), want[(300, None)][1])
+        # profiling mode: graphs with an event node on either side of every kernel, same bits, and the
+        # per-kernel times of each replay (one launch of every kernel per batch)
+        h.profile(True)
+        h.profile_read(reset=True)
+        for rep in range(3):
+            r = h.batch(Y[:300], prob.S)
+            if rep == 1:
+                h.profile_read(reset=False)       # read between replays; the third is collected lazily
+            got = _fields(r)
+            for a, b in zip(got, want[(300, None)]):
+                assert np.array_equal(a, b), ("profiled", rep)
+        prof = h.profile_read(reset=True)
+        h.profile(False)
+        assert prof["correlation"][1] == 3 * prob.S and prof["update"][1] == 3 * prob.S
+        assert prof["init"][1] == 3 and prof["update"][0] > 0 and prof["correlation"][0] > 0
 
 
 def test_host_path_matches_device_path():
