@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     for (int q = tid; q < f4; q += T) cp_async16(reinterpret_cast<float4*>(Fs) + q, fg + q);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+#ifndef OMP_NO_FPF
   if constexpr (!FSM) {
     const char* fp = reinterpret_cast<const char*>(a.F + b * a.ldf);
     // (only while F_k fits L1 comfortably; a large one is read from L2 with loads in flight instead)
@@ -134,11 +135,14 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     for (uint32_t o = (uint32_t)tid * 128u; o < fbytes; o += (uint32_t)T * 128u)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
   }
+#endif
+#ifndef OMP_NO_YPF
   {
     const char* yp = reinterpret_cast<const char*>(a.Y + b * a.ldy);
     for (int64_t o = (int64_t)tid * 128; o < a.M * 4; o += (int64_t)T * 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
   }
+#endif
 
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
