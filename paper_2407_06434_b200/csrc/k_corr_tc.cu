@@ -258,7 +258,10 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     }
   }
   fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  // (the CTA barrier after the cluster barrier also orders the TMEM address tcgen05.alloc wrote to
+  // shared memory for compute-sanitizer's racecheck, which does not model barrier.cluster)
+  if constexpr (CG == 2) cluster_sync();
+  __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

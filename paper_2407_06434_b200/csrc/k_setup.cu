@@ -50,7 +50,7 @@ __device__ __forceinline__ double block_sum_double(double v, double* red) {
 __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t N, int64_t lda, int64_t Mp,
                                  float* __restrict__ At, __nv_bfloat16* __restrict__ Ab, float* __restrict__ Ahi,
                                  float* __restrict__ Alo, float* __restrict__ norm, float* __restrict__ inv_norm,
-                                 int* bad_zero, int* bad_nonfinite) {
+                                 int* bad_zero, int* bad_nonfinite, unsigned long long* ea2_max) {
   __shared__ double red[32];
   const int64_t n = blockIdx.x;
   double ss = 0.0;
@@ -65,10 +65,21 @@ __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t
   ss = block_sum_double(ss, red);
   const bool ok = n < N && ss > 0.0 && !any_bad;
   const float inv = ok ? (float)(1.0 / sqrt(ss)) : 0.f;
+  // E_a: ||bf16(a_n * (1/||a_n||)) - a_n / ||a_n|||| in FP64, the screen's atom error
+  const double rs = ok ? 1.0 / sqrt(ss) : 0.0;
+  double e2 = 0.0;
   for (int64_t m = threadIdx.x; m < Mp; m += blockDim.x) {
     const float v = (n < N && m < M) ? A[n * lda + m] : 0.f;
     At[n * Mp + m] = v;
     put_planes(n * Mp + m, v * inv, nullptr, Ab, Ahi, Alo);
+    if (Ab) {
+      const double d = (double)__bfloat162float(__float2bfloat16_rn(v * inv)) - (double)v * rs;
+      e2 += d * d;
+    }
+  }
+  if (Ab && ea2_max) {
+    e2 = block_sum_double(e2, red);
+    if (threadIdx.x == 0 && n < N) atomicMax(ea2_max, (unsigned long long)__double_as_longlong(e2));
   }
   if (threadIdx.x == 0) {
     if (n < N) {
@@ -82,9 +93,10 @@ __global__ void k0_prepare_atoms(const float* __restrict__ A, int64_t M, int64_t
 
 cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
                                  float* At, void* At_bf16, float* At_hi, float* At_lo, float* norm,
-                                 float* inv_norm, int* bad_zero, int* bad_nonfinite, cudaStream_t st) {
+                                 float* inv_norm, int* bad_zero, int* bad_nonfinite, unsigned long long* ea2_max,
+                                 cudaStream_t st) {
   k0_prepare_atoms<<<(unsigned)Np, 128, 0, st>>>(A, M, N, lda, Mp, At, (__nv_bfloat16*)At_bf16, At_hi, At_lo,
-                                                 norm, inv_norm, bad_zero, bad_nonfinite);
+                                                 norm, inv_norm, bad_zero, bad_nonfinite, ea2_max);
   return cudaGetLastError();
 }
 
@@ -112,21 +124,27 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
                              float* __restrict__ Rlo, float* __restrict__ X, int64_t ldx,
                              int32_t* __restrict__ support, int64_t lds, float* __restrict__ resid,
                              int32_t* __restrict__ n_iter, int32_t* __restrict__ status, int32_t* __restrict__ slot,
-                             int32_t* __restrict__ live0, float* __restrict__ rslot, double* __restrict__ ynorm2) {
+                             int32_t* __restrict__ live0, float* __restrict__ rslot, double* __restrict__ ynorm2,
+                             WinCoef win) {
   __shared__ double red[32];
   __shared__ int s_slot;
   const int64_t b = blockIdx.x;
   const float* y = Y + b * ldy;
-  float part = 0.f;
+  float part = 0.f, dpart = 0.f;
   for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
     const float v = y[m];
     part = fmaf(v, v, part);
+    if (Rb) {                 // the bf16 plane's rounding error (exact difference), for the window
+      const float d = v - __bfloat162float(__float2bfloat16_rn(v));
+      dpart = fmaf(d, d, dpart);
+    }
   }
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     X[b * ldx + j] = 0.f;
     support[b * lds + j] = -1;
   }
   const double ss = block_sum_double((double)part, red);
+  const double dd = (Rb && live0) ? block_sum_double((double)dpart, red) : 0.0;
   if (threadIdx.x == 0) {
     const float rn = (float)sqrt(ss);
     if (ynorm2) ynorm2[b] = ss;
@@ -144,7 +162,9 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
     if (st == SIG_RUNNING) {
       if (live0) {
         s_slot = atomicAdd(live0, 1);
-        rslot[s_slot] = rn;
+        // the first screen's window W_b; d rounded up over its FP32 partial sums
+        const float dn = (float)sqrt(dd) * (1.f + 0x1p-10f);
+        rslot[s_slot] = fmaf(win.ca, rn + dn, fmaf(win.cd, dn, win.cr * rn));
       } else {
         s_slot = (int)b;                  // small-batch path: no compaction
       }
@@ -161,10 +181,11 @@ __global__ void k_batch_init(const float* __restrict__ Y, int64_t ldy, int64_t M
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
-                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st, double* ynorm2) {
+                              int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st, double* ynorm2,
+                              WinCoef win) {
   if (B == 0) return cudaSuccess;
   k_batch_init<<<(unsigned)B, 128, 0, st>>>(Y, ldy, M, Mp, S, eps, R32, (__nv_bfloat16*)Rb, R_hi, R_lo, X, ldx,
-                                            support, lds, resid, n_iter, status, slot, live0, rslot, ynorm2);
+                                            support, lds, resid, n_iter, status, slot, live0, rslot, ynorm2, win);
   return cudaGetLastError();
 }
 

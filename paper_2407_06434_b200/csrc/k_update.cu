@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
 
   // ---- issue every load that does not depend on the selection (one round trip instead of a chain):
   // support and u of the current factor and (REFINE) the residual row -> shared memory by cp.async;
-  // F_k -> L1 (both passes of the append read it); y -> L2 (the residual phase reads it)
+  // F_k -> L1 (both passes of the append read it)
   for (int j = tid; j < k; j += T) {
     cp_async4(&ss[j], a.support + b * a.lds + j);
     cp_async4(&u[j], a.U + b * a.ldu + j);
@@ -136,13 +136,8 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
   }
 #endif
-#ifndef OMP_NO_YPF
-  {
-    const char* yp = reinterpret_cast<const char*>(a.Y + b * a.ldy);
-    for (int64_t o = (int64_t)tid * 128; o < a.M * 4; o += (int64_t)T * 128)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(yp + o));
-  }
-#endif
+  // (no L2 prefetch of y: measured at c4, its lines are evicted before the residual phase reads them
+  // -- 0.84 GB of extra DRAM reads per launch for 0.8 GB of y, and 1.2 % slower; profiles/r02/ab_dram)
 
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
@@ -169,7 +164,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
       if (tid == 0) a.status[b] = OMP_SIG_DEGENERATE;
       return;
     }
-    const float thr = vmax - a.window * rn;
+    const float thr = vmax - a.rslot_in[cur_slot];       // the window W of this signal
     bool full = false;
     for (int t = tid; t < a.groups; t += T) {
       const float2 last = Pt[t * TOPK + TOPK - 1];
@@ -370,7 +365,7 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
   UpdateArgs a;
   a.k = L.k; a.S = L.S; a.eps = L.eps; a.N = L.N; a.M = L.M; a.Mp = L.Mp;
-  a.part = L.part; a.groups = L.groups; a.window = L.window; a.nstar = L.nstar; a.cstar = L.cstar;
+  a.part = L.part; a.groups = L.groups; a.rslot_in = L.rslot_in; a.win = L.win; a.nstar = L.nstar; a.cstar = L.cstar;
   a.At = L.At; a.inv_norm = L.inv_norm; a.G = L.G; a.ldg = L.ldg;
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;
   a.support = L.support; a.lds = L.lds; a.R32in = L.R32in; a.R32 = L.R32; a.Rb = (__nv_bfloat16*)L.Rb;

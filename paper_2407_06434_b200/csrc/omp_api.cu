@@ -49,7 +49,10 @@ struct ompHandle_st {
   int device = 0;
   int64_t M = 0, N = 0, Mp = 0, Np = 0;
   int mode = OMP_CORR_3XTF32;
-  float window = 0.f;      // screening window / ||r|| (tensor-core modes), DESIGN.md §5
+  float window = 0.f;      // static screening window / ||r|| (tensor-core modes), DESIGN.md §5
+  WinCoef win{0.f, 0.f, 0.f};  // the per-signal window's coefficients (WinCoef)
+  double ea = 0.0;         // E_a = max_n ||bf16(a_n / ||a_n||) - a_n / ||a_n|||| (bf16 mode)
+  unsigned long long* dea2 = nullptr;
   size_t l2_persist = 0;   // bytes of At under a persisting L2 access-policy window (0: off)
   bool persist_ref = false; // this handle holds a reference on the device's persisting-L2 limit
   // dictionary (owned): FP32 copy of A^T (Np x Mp), the screen's plane(s), 1/||a_n||, Gram
@@ -498,7 +501,8 @@ static ompStatus_t enqueue_screened(ompHandle_t h, const WsView& w, const float*
   if (e != cudaSuccess) return cuda_fail(h, e);
   L.begin(0);
   e = launch_batch_init(Y, B, ldy, h->M, h->Mp, S, eps, w.R32[0], w.Rb[0], w.Rhi[0], w.Rlo[0],
-                        X, ldx, support, lds, resid, n_iter, status, w.slot, w.live, w.rslot[0], st);
+                        X, ldx, support, lds, resid, n_iter, status, w.slot, w.live, w.rslot[0], st, nullptr,
+                        h->win);
   L.end(0);
   if (e != cudaSuccess) return cuda_fail(h, e);
   const Operand At = atoms_operand(h);
@@ -507,10 +511,9 @@ static ompStatus_t enqueue_screened(ompHandle_t h, const WsView& w, const float*
     const Operand R = view_operand(h, w, B, cur);
     if (tc_mode(h)) {
       // a2: tensor-core screen C~ = A^T R_k over the live rows; the epilogue keeps the in-window
-      // entries of every 128-atom group
+      // entries of every 128-atom group (rslot holds each row's absolute window W_b)
       L.begin(1);
-      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, w.live + k, w.rslot[cur], h->window,
-                              w.part, st);
+      e = launch_corr_tc_topk(tc_kind(h), R, At, h->Mp, w.live + k, w.rslot[cur], 1.0f, w.part, st);
       L.end(1);
       if (e == cudaErrorNotSupported) return OMP_ERR_UNSUPPORTED;
       if (e != cudaSuccess) return cuda_fail(h, e);
@@ -531,7 +534,8 @@ static ompStatus_t enqueue_screened(ompHandle_t h, const WsView& w, const float*
     U.k = k; U.S = S; U.eps = eps; U.B = B; U.N = h->N; U.M = h->M; U.Mp = h->Mp;
     U.part = tc_mode(h) ? w.part : nullptr;
     U.groups = (int)(h->Np / SCREEN_GROUP);
-    U.window = h->window;
+    U.rslot_in = w.rslot[cur];
+    U.win = h->win;
     U.nstar = w.nstar; U.cstar = w.cstar;
     U.At = h->At; U.inv_norm = h->inv_norm; U.G = h->G; U.ldg = h->Np;
     U.Y = Y; U.ldy = ldy; U.F = w.F; U.ldf = h->ldf; U.U = w.U; U.ldu = h->ldu; U.X = X; U.ldx = ldx;
@@ -790,6 +794,7 @@ ompStatus_t ompDestroy(ompHandle_t h) {
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->At); dfree(h->At_hi); dfree(h->At_lo); dfree(h->Ab); dfree(h->norm); dfree(h->inv_norm); dfree(h->G);
     dfree(h->dflags);
+    dfree(h->dea2);
     dfree(h->pbest);
     dfree(h->gbar);
     dfree(h->R32); dfree(h->R_hi); dfree(h->R_lo); dfree(h->Rb); dfree(h->C); dfree(h->F); dfree(h->U);
@@ -855,7 +860,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   }
   const size_t plane = (size_t)h->Np * h->Mp;
   bool ok = dalloc(h->At, plane) && dalloc(h->inv_norm, (size_t)h->Np) && dalloc(h->norm, (size_t)h->Np) && dalloc(h->G, (size_t)h->Np * h->Np) &&
-            dalloc(h->dflags, 2);
+            dalloc(h->dflags, 2) && dalloc(h->dea2, 1);
   if (ok && corr_mode == OMP_CORR_BF16) ok = dalloc(h->Ab, plane);
   if (ok && corr_mode == OMP_CORR_3XTF32) ok = dalloc(h->At_hi, plane) && dalloc(h->At_lo, plane);
   if (!ok) {
@@ -865,11 +870,14 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
   }
   int init_flags[2] = {INT_MAX, INT_MAX};
   cudaError_t e = cudaMemcpyAsync(h->dflags, init_flags, sizeof(init_flags), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->dea2, 0, sizeof(unsigned long long), st);
   if (e == cudaSuccess)
     e = launch_prepare_atoms(A, M, N, lda, h->Mp, h->Np, h->At, h->Ab, h->At_hi, h->At_lo, h->norm, h->inv_norm,
-                             h->dflags, h->dflags + 1, st);
+                             h->dflags, h->dflags + 1, h->dea2, st);
   int flags[2] = {INT_MAX, INT_MAX};
+  unsigned long long ea2_bits = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(flags, h->dflags, sizeof(flags), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&ea2_bits, h->dea2, sizeof(ea2_bits), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     ompStatus_t s = cuda_fail(nullptr, e);
@@ -881,6 +889,19 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
     g_create_detail = nonfinite ? flags[1] : flags[0];
     ompDestroy(h);
     return nonfinite ? OMP_ERR_NONFINITE : OMP_ERR_ZERO_COLUMN;
+  }
+  {
+    // window coefficients (WinCoef), every term rounded up into FP32
+    double ea2 = 0.0;
+    memcpy(&ea2, &ea2_bits, sizeof(ea2));
+    h->ea = sqrt(ea2) * (1.0 + 1e-12);
+    const double u23 = ldexp(1.0, -23), Kp = (double)h->Mp;
+    const double c_ref = (Kp / 32.0 + 8.0) * u23;
+    auto up = [](double v) { return nextafterf((float)v, INFINITY); };
+    if (corr_mode == OMP_CORR_BF16)
+      h->win = WinCoef{up(2.5 * (h->ea + Kp * u23 * (1.0 + h->ea))), up(2.5), up(2.5 * c_ref)};
+    else if (corr_mode == OMP_CORR_3XTF32)
+      h->win = WinCoef{0.f, 0.f, up((double)h->window)};
   }
   // Gram matrix G = A^T A in FP32 with round-to-nearest accumulation (the
   // truncating tensor-core accumulator would bias ||a||^2 - ||z||^2)

@@ -43,6 +43,16 @@ inline bool pdl_enabled(int edge) {
   return (on & edge) != 0;
 }
 
+// The screen's candidate window per signal, in absolute units:
+//   W_b = ca (||r_b|| + d_b) + cd d_b + cr ||r_b||,   d_b = ||r_b - bf16(r_b)|| (measured when the
+// residual's bf16 plane is written; 0 without a bf16 plane).  bf16 screen: ca = 2.5 (E_a + K 2^-23
+// (1 + E_a)) with E_a = max_n ||bf16(a_n / ||a_n||) - a_n / ||a_n||||, cd = 2.5, cr = 2.5 c0' (the FP32
+// re-evaluation); 3xTF32 screen: ca = cd = 0, cr = the static window 2.5 (c0 + c0').  Stored per live
+// row in rslot (the screen's and the refine's threshold is max - W_b).
+struct WinCoef {
+  float ca, cd, cr;
+};
+
 // screening-GEMM operand kinds
 constexpr int KIND_BF16 = 0;
 constexpr int KIND_3XTF32 = 1;
@@ -92,20 +102,23 @@ cudaError_t launch_select(const float* C, int64_t ldc, int64_t B, int64_t N, con
 // ---- setup / init ----
 // K0: atoms -> FP32 copy At (Np x Mp), ||a_n||, 1/||a_n||, and the screen planes of the NORMALISED
 // atoms a_n / ||a_n|| (optional bf16 plane / tf32 hi-lo planes)
+// ea2_max (bf16 plane only): max over atoms of ||bf16(a_n / ||a_n||) - a_n / ||a_n||||^2 in FP64, as the
+// bits of a non-negative double (atomicMax on unsigned long long); zero it before the launch
 cudaError_t launch_prepare_atoms(const float* A, int64_t M, int64_t N, int64_t lda, int64_t Mp, int64_t Np,
                                  float* At, void* At_bf16, float* At_hi, float* At_lo, float* norm,
-                                 float* inv_norm, int* bad_zero, int* bad_nonfinite, cudaStream_t st);
+                                 float* inv_norm, int* bad_zero, int* bad_nonfinite,
+                                 unsigned long long* ea2_max, cudaStream_t st);
 // row-major fp32 matrix -> padded planes (fp32 copy, optional bf16, optional hi/lo)
 cudaError_t launch_make_planes(const float* R, int64_t B, int64_t ldr, int64_t M, int64_t Mp, float* R32,
                                void* Rb, float* R_hi, float* R_lo, cudaStream_t st);
 // a1: batch init; running signals take live-set slots (atomic counter *live0) and their r_0 = y
-// planes go to row slot[b]; rslot[slot] = ||y||.  live0 == nullptr: no compaction, row b (slot and
-// rslot may then be null).
+// planes go to row slot[b]; rslot[slot] = the window W_b of r_0 = y (WinCoef).  live0 == nullptr: no
+// compaction, row b (slot and rslot may then be null).
 cudaError_t launch_batch_init(const float* Y, int64_t B, int64_t ldy, int64_t M, int64_t Mp, int32_t S,
                               float eps, float* R32, void* Rb, float* R_hi, float* R_lo, float* X, int64_t ldx,
                               int32_t* support, int64_t lds, float* resid, int32_t* n_iter, int32_t* status,
                               int32_t* slot, int32_t* live0, float* rslot, cudaStream_t st,
-                              double* ynorm2 = nullptr);
+                              double* ynorm2 = nullptr, WinCoef win = WinCoef{0.f, 0.f, 0.f});
 // projection path: exact ||y - A_S x|| per signal after the last iteration
 cudaError_t launch_final_resid(const float* Y, int64_t B, int64_t ldy, int64_t M, const float* At, int64_t Mp,
                                const float* X, int64_t ldx, const int32_t* support, int64_t lds,
@@ -118,7 +131,8 @@ struct UpdateLaunch {
   int64_t B, N, M, Mp;
   const float2* part;      // screen partials (tensor-core modes) or nullptr (then nstar/cstar are used)
   int groups;              // screen partial groups per row (Np / SCREEN_GROUP)
-  float window;
+  const float* rslot_in;   // the window W of each row of this iteration's buffer (refine threshold)
+  WinCoef win;             // the next window's coefficients
   const int32_t* nstar;
   const float* cstar;
   const float* At;
@@ -140,7 +154,7 @@ struct UpdateLaunch {
   void* Rb;
   float* Rhi;
   float* Rlo;
-  float* rslot_out;        // ||r|| per new slot (the next screen's window)
+  float* rslot_out;        // window W per new slot (the next screen's and refine's threshold)
   int32_t* slot;           // signal -> row of the current buffer; updated to the new slot
   int32_t* live_next;      // atomic slot counter of the next buffer
   float* resid;

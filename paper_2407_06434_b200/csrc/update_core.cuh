@@ -39,7 +39,8 @@ struct UpdateArgs {
   // selection inputs
   const float2* part;   // screen partials (REFINE)
   int groups;           // screen partial groups per row (Np / SCREEN_GROUP)
-  float window;
+  const float* rslot_in;  // window W of each row of the current buffer (REFINE)
+  WinCoef win;          // coefficients of the next window (written to rslot_out)
   const int32_t* nstar; // preselected (SIMT mode)
   const float* cstar;
   // dictionary
@@ -206,7 +207,8 @@ struct TailSmem {
   int* ss;
   uint32_t* ro;   // atom row offsets (float4 units) for the gather
   float* red;     // T / 32 floats
-  float* pr;      // Mp / 4 floats: per-chunk partials of ||r||^2
+  float* pr;      // Mp / 4 floats: per-chunk partials of ||r||^2 (and, with a bf16 plane, Mp / 4 more:
+                  // per-chunk partials of ||r - bf16(r)||^2)
   int* bcast;     // one int
 };
 
@@ -479,10 +481,20 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       }
       acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);   // r
       // ||r||^2: one partial per float4 chunk, summed below in an order that does not depend on T
-      if constexpr (!V0) sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));
+      if constexpr (!V0) {
+        sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));
+        if (a.Rb) {   // the bf16 plane's rounding error, for the next window (exact differences)
+          const float4 e = make_float4(acc[c].x - __bfloat162float(__float2bfloat16_rn(acc[c].x)),
+                                       acc[c].y - __bfloat162float(__float2bfloat16_rn(acc[c].y)),
+                                       acc[c].z - __bfloat162float(__float2bfloat16_rn(acc[c].z)),
+                                       acc[c].w - __bfloat162float(__float2bfloat16_rn(acc[c].w)));
+          sm.pr[q4 + q] = fmaf(e.x, e.x, fmaf(e.y, e.y, fmaf(e.z, e.z, e.w * e.w)));
+        }
+      }
     }
   }
   float rr;
+  float dn2 = 0.f;                      // ||r - bf16(r)||^2 (bf16 plane only; warp 0)
   if constexpr (V0) {
     // ||r_{k+1}||^2 = ||y||^2 - ||u_{k+1}||^2 (q_j orthonormal, u_j = q_j^T y, pin P9),
     // in FP64.  The u_j carry FP32 errors, so where this estimate is within 1e-5 ||y||^2 of eps^2 the
@@ -508,11 +520,18 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   } else {
     __syncthreads();
     rr = 0.f;
+    float dd = 0.f;
     if (warp == 0) {                    // lane l: chunks l, l + 32, ... ascending, then the xor tree
       for (int q = lane; q < q4; q += 32) rr += sm.pr[q];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+      if (a.Rb) {
+        for (int q = lane; q < q4; q += 32) dd += sm.pr[q4 + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+      }
     }
+    dn2 = dd;
   }
   OMP_TAIL_TRACE(5);
   if (tid == 0) {
@@ -524,7 +543,10 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     else if (kk == a.S) a.status[b] = OMP_SIG_MAXITER;
     else if (a.live_next) {
       ns = atomicAdd(a.live_next, 1);                                  // next live-set slot
-      a.rslot_out[ns] = rn;
+      // the next screen's window: d = ||r - bf16(r)|| rounded up (its FP32 sum of
+      // squares is off by < 2^-17 relative: the 1 + 2^-10 margin covers it)
+      const float dn = a.Rb ? sqrtf(dn2) * (1.f + 0x1p-10f) : 0.f;
+      a.rslot_out[ns] = fmaf(a.win.ca, rn + dn, fmaf(a.win.cd, dn, a.win.cr * rn));
     } else {
       ns = (int)b;                                                     // no compaction: row b
     }

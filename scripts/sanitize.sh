@@ -10,7 +10,6 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ $tool = memcheck ] && extra="--leak-check full"
-  [ $tool = initcheck ] && extra="--track-unused-memory no"
   for paths in "bf16 3xtf32 simt small proj host densify correlate" "proj_simt"; do
     echo "=== $tool: $paths" >> $OUT/sanitize_${TAG}_${tool}.txt
     if [ "$paths" = proj_simt ]; then envp="OMP_B200_P0=simt"; else envp=""; fi

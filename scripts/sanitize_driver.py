@@ -81,6 +81,14 @@ def main(paths):
         for (M, N, B, S) in ((32, 64, 16, 4), (256, 1024, 300 if path != "small" else 12, 32)):
             run(path, M, N, B, S, 7)
         print(f"sanitize_driver: {path} ok", flush=True)
+    # every library handle is destroyed by now; hand torch's cached device / pinned blocks back too, so
+    # memcheck --leak-check full reports only what the library itself might have leaked
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    if hasattr(torch._C, "_host_emptyCache"):
+        torch._C._host_emptyCache()
 
 
 if __name__ == "__main__":

@@ -84,3 +84,45 @@ def test_library_window_values(window):
         assert window("bf16", M) == pytest.approx(bf, rel=1e-6)
         assert window("3xtf32", M) == pytest.approx(x3, rel=1e-6)
         assert window("simt", M) == -1.0
+
+
+def adaptive_window(A32, y32, M):
+    """The per-signal window the library uses in bf16 mode (WinCoef):
+    W = 2.5 (E_a (|r| + d) + d + K 2^-23 (1 + E_a)(|r| + d) + c0' |r|), E_a = max_n |bf16(a_n/|a_n|) - a_n/|a_n||,
+    d = |r - bf16(r)| -- both measured on the actual operands (here emulated exactly)."""
+    A64 = A32.astype(np.float64)
+    ss = np.sum(A64 ** 2, axis=0)
+    inv = (1.0 / np.sqrt(ss)).astype(np.float32)
+    ahat32 = (A32 * inv[None, :]).astype(np.float32)
+    Ea = np.max(np.linalg.norm(bf16_rn(ahat32) - A64 / np.sqrt(ss)[None, :], axis=0))
+    r = y32.astype(np.float64)
+    rn = np.linalg.norm(r)
+    d = np.linalg.norm(r - bf16_rn(y32))
+    Kp = -(-M // 64) * 64
+    u = 2.0 ** -23
+    return 2.5 * (Ea * (rn + d) + d + Kp * u * (1 + Ea) * (rn + d) + (Kp / 32 + 8) * u * rn), Ea, d / rn
+
+
+@pytest.mark.parametrize("M,seed,swap", CASES)
+def test_adaptive_window_covers_the_adversary(window, M, seed, swap):
+    """The measured-rounding window widens on adversarial operands (E_a, d/|r| near 2^-8) and still
+    covers the screen's lead; it never exceeds the static worst case (ompScreeningWindow)."""
+    A, y, _ = make_screen_adversary(M, seed, swap)
+    win, lose = (1, 0) if swap else (0, 1)
+    v = emulated_screen(A, y)
+    rn = float(np.linalg.norm(y.astype(np.float64)))
+    lead = (v[lose] - v[win]) / rn
+    W, Ea, drel = adaptive_window(A, y, M)
+    assert Ea > 0.9 * 2.0 ** -8 and drel > 0.9 * 2.0 ** -8      # the operands err almost maximally
+    assert lead < W / rn <= window("bf16", M) * (1 + 1e-6)
+
+
+def test_adaptive_window_is_narrower_on_gaussian_data(window):
+    """On the configs' Gaussian data the measured rounding is ~2.3x below the worst case, so the
+    per-signal window is about half the static bound (fewer FP32 re-evaluations)."""
+    from synth import make_problem
+    prob = make_problem("c2", B=8)
+    for y in prob.Y:
+        W, Ea, drel = adaptive_window(prob.A, y, prob.M)
+        rn = float(np.linalg.norm(y.astype(np.float64)))
+        assert 0.3 < (W / rn) / window("bf16", prob.M) < 0.6
