@@ -46,6 +46,7 @@ namespace ompb {
 #define OMP_RF_CAP 512
 #endif
 constexpr int RF_CAP = OMP_RF_CAP;   // explicit candidate list capacity (beyond: all N atoms)
+constexpr int GRP_CAP = 64;          // overflowing 128-atom groups re-evaluated whole (beyond: all N)
 constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared memory
 // columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
 // cost registers and lose at c4 and at c5 B = 10^5)
@@ -102,10 +103,15 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   __shared__ float red[T / 32];
   __shared__ Cand red_c[T / 32];
   __shared__ int ncand;
+  __shared__ int ngrp;                 // overflowing screen groups inside the window (re-evaluated whole)
+  __shared__ int grp[GRP_CAP];
   __shared__ int sel_n;
   __shared__ float sel_c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) ncand = 0;
+  if (tid == 0) {
+    ncand = 0;
+    ngrp = 0;
+  }
 
   // ---- issue every load that does not depend on the selection (one round trip instead of a chain):
   // support and u of the current factor and (REFINE) the residual row -> shared memory by cp.async;
@@ -170,13 +176,10 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
       const float2 last = Pt[t * TOPK + TOPK - 1];
       const int nl = __float_as_int(last.y);
       if (nl == SEL_OVERFLOW && last.x >= thr) {         // more in-window entries than kept: all of it
-        const int n0 = t * SCREEN_GROUP;
-        const int cnt = (int)min((int64_t)SCREEN_GROUP, a.N - n0);
-        if (cnt > 0) {
-          const int at = atomicAdd(&ncand, cnt);
-          if (at + cnt > RF_CAP) full = true;
-          else
-            for (int i = 0; i < cnt; ++i) cand[at + i] = n0 + i;
+        if ((int64_t)t * SCREEN_GROUP < a.N) {
+          const int at = atomicAdd(&ngrp, 1);
+          if (at >= GRP_CAP) full = true;
+          else grp[at] = t;
         }
       } else {
         for (int j = 0; j < TOPK; ++j) {
@@ -196,17 +199,27 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     UPD_TRACE(1);
 #ifdef OMP_UPDATE_TRACE
     if (tid == 0 && a.k == g_upd_trace_k) {   // candidate statistics: sum, > 16, > 128, full fallback
-      atomicAdd(&g_upd_clk[12], (unsigned long long)min(ncand, RF_CAP));
-      if (ncand > 16) atomicAdd(&g_upd_clk[13], 1ull);
-      if (ncand > 128) atomicAdd(&g_upd_clk[14], 1ull);
+      const int nc = min(ncand, RF_CAP) + min(ngrp, GRP_CAP) * SCREEN_GROUP;
+      atomicAdd(&g_upd_clk[12], (unsigned long long)nc);
+      if (nc > 16) atomicAdd(&g_upd_clk[13], 1ull);
+      if (ngrp > 0) atomicAdd(&g_upd_clk[14], 1ull);
       if (full) atomicAdd(&g_upd_clk[3], 1ull);
     }
 #endif
     Cand best{-1.f, 0x7fffffff, 0.f};
     bool nan_c = false;
-    const int count = full ? (int)a.N : min(ncand, RF_CAP);
+    // the kept entries, then every atom of each overflowing group (no atom is in both); more than the
+    // lists hold: all N atoms
+    const int nind = min(ncand, RF_CAP), ng = min(ngrp, GRP_CAP);
+    const int count = full ? (int)a.N : nind + ng * SCREEN_GROUP;
     for (int j = warp; j < count; j += T / 32) {
-      const int n = full ? j : cand[j];
+      int n;
+      if (full) n = j;
+      else if (j < nind) n = cand[j];
+      else {
+        n = grp[(j - nind) / SCREEN_GROUP] * SCREEN_GROUP + (j - nind) % SCREEN_GROUP;
+        if (n >= a.N) continue;                        // the last group's padding (warp-uniform)
+      }
       const float c = warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane);
       nan_c |= isnan(c);
       const Cand cd{fabsf(c) * a.inv_norm[n], n, c};

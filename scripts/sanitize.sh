@@ -20,6 +20,6 @@ for tool in memcheck racecheck synccheck initcheck; do
   grep -E "ERROR SUMMARY|LEAK SUMMARY|RACECHECK SUMMARY|=== rc|sanitize_driver" $OUT/sanitize_${TAG}_${tool}.txt
 done
 OMP_B200_DEBUG_FILL=1 timeout 1200 python -m pytest tests -m gpu -q -x \
-  -k "tiny or c2_all or ragged or edge or worked or graph or host_path or strided or adversarial or falls_back" \
+  -k "tiny or c2_all or ragged or edge or worked or graph or host_path or strided or adversarial or overflowing" \
   > $OUT/sanitize_${TAG}_debugfill_pytest.txt 2>&1
 echo "debug-fill pytest rc=$?"; tail -2 $OUT/sanitize_${TAG}_debugfill_pytest.txt

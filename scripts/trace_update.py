@@ -58,7 +58,7 @@ def main():
         print(f"{cfg} B={B} k={k}: {int(n)} CTAs, {tot:.0f} cycles per CTA")
         for p, name in PHASES.items():
             print(f"   {name:20s} {v[p] / n:9.0f}  {100 * v[p] / n / tot:5.1f} %")
-        print(f"   candidates: mean {v[12] / n:.2f}, > 16: {int(v[13])}, > 128: {int(v[14])}, "
+        print(f"   candidates: mean {v[12] / n:.2f}, > 16: {int(v[13])}, with an overflowing group: {int(v[14])}, "
               f"all-N fallback: {int(v[3])} of {int(n)} signals")
 
 

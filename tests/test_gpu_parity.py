@@ -284,20 +284,23 @@ def test_screen_window_adversarial_rounding(mode):
         assert d["counts"].get("exact", 0) == 2
 
 
+@pytest.mark.parametrize("copies", [1, 16], ids=["groups", "all-N"])
 @pytest.mark.parametrize("mode", ["bf16", "3xtf32"])
-def test_refine_falls_back_to_all_atoms(mode):
-    """More than RF_CAP = 512 candidates inside the window: 600 exactly tied atoms (identity
-    dictionary, M = N = 1024, y = sum of 600 unit vectors) fill every 128-atom screen group past its
-    4 kept entries, so all 8 groups (1024 atoms) are candidates and the update re-evaluates all N
-    atoms.  Exact ties -> lowest index (reading R4): the selections are the tied atoms in ascending
-    order, every coefficient exactly 1, ||r||^2 = 600 - S exactly.  Then a random orthonormal
-    dictionary with the same structure (ties to ~1e-7, all inside the window): bitwise equal to the
-    small-batch kernel, which evaluates every atom exactly."""
-    M = N = 1024
+def test_refine_overflowing_groups_and_all_atoms(mode, copies):
+    """Exact ties filling the screen's groups: the dictionary is `copies` side-by-side copies of the
+    identity (M = 1024), y = the sum of 600 unit vectors, so every 128-atom group holds ~75 tied
+    entries -- more than its 4 kept slots -- and is re-evaluated whole: 8 groups for one copy; 128
+    groups for 16 copies, more than the 64-group list holds, so the update re-evaluates all N = 16 384
+    atoms.  Exact ties -> lowest index (reading R4): the tied atoms of the first copy in ascending
+    order, every coefficient exactly 1, ||r||^2 = 600 - S exactly.  Then (one copy) a random orthonormal
+    dictionary with the same structure (ties to ~1e-7): bitwise equal to the small-batch kernel, which
+    evaluates every atom exactly."""
+    M = 1024
+    N = M * copies
     S, B = 16, 16
     rng = np.random.default_rng(5)
-    T = [np.sort(rng.choice(N, 600, replace=False)) for _ in range(B)]
-    A = np.eye(M, dtype=np.float32)
+    T = [np.sort(rng.choice(M, 600, replace=False)) for _ in range(B)]
+    A = np.tile(np.eye(M, dtype=np.float32), (1, copies))
     Y = np.zeros((B, M), dtype=np.float32)
     for b in range(B):
         Y[b, T[b]] = 1.0
@@ -309,6 +312,8 @@ def test_refine_falls_back_to_all_atoms(mode):
     assert np.all(scr["resid"] == np.float32(np.sqrt(600 - S)))
     for key in ("support", "X", "resid", "n_iter", "status"):
         assert np.array_equal(scr[key], small[key]), key
+    if copies > 1:
+        return
     Q = np.linalg.qr(rng.standard_normal((M, M)))[0].astype(np.float32)
     Yq = np.stack([Q[:, T[b]].astype(np.float64).sum(axis=1) for b in range(B)]).astype(np.float32)
     scr = run_gpu(Q, Yq, S, None, mode)
