@@ -342,6 +342,13 @@ static ompStatus_t ensure_workspace(ompHandle_t h, int64_t B, int32_t S) {
     cudaGetLastError();
     return OMP_ERR_NOMEM;
   }
+  // the packed factors are staged into shared memory in whole 16-byte chunks, so a copy may read up to
+  // 3 floats past the columns written so far (never used): start them defined (compute-sanitizer
+  // initcheck), once per allocation
+  if (cudaMemset(h->F, 0, (size_t)nB * ldf * sizeof(float)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    return OMP_ERR_CUDA;
+  }
   h->capB = nB;
   h->capS = nS;
   h->ldf = ldf;

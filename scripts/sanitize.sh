@@ -19,6 +19,14 @@ for tool in memcheck racecheck synccheck initcheck; do
   done
   grep -E "ERROR SUMMARY|LEAK SUMMARY|RACECHECK SUMMARY|=== rc|sanitize_driver" $OUT/sanitize_${TAG}_${tool}.txt
 done
+# the screen with single-SM UMMA (no cluster mbarrier traffic between CTA pairs): racecheck's hazards on
+# the 2-CTA kernel are between mbarrier instructions (SYNCS try_wait / remote arrive) only
+echo "=== racecheck cta_group::1: bf16 3xtf32" >> $OUT/sanitize_${TAG}_racecheck_cg1.txt
+OMP_B200_CTA_GROUP=1 timeout 1500 $CS --tool racecheck --error-exitcode 17 python scripts/sanitize_driver.py bf16 3xtf32 \
+  >> $OUT/sanitize_${TAG}_racecheck_cg1.txt 2>&1
+echo "=== rc=$?" >> $OUT/sanitize_${TAG}_racecheck_cg1.txt
+grep -E "RACECHECK SUMMARY|=== rc" $OUT/sanitize_${TAG}_racecheck_cg1.txt
+python scripts/sanitize_summary.py $OUT/sanitize_${TAG}_*.txt
 OMP_B200_DEBUG_FILL=1 timeout 1200 python -m pytest tests -m gpu -q -x \
   -k "tiny or c2_all or ragged or edge or worked or graph or host_path or strided or adversarial or overflowing" \
   > $OUT/sanitize_${TAG}_debugfill_pytest.txt 2>&1
