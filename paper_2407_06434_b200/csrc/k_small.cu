@@ -360,7 +360,7 @@ cudaError_t launch_small(const UpdateLaunch& L, float4* pbest, unsigned int* bar
   SmallArgs s;
   UpdateArgs& a = s.a;
   a.k = 0; a.S = L.S; a.fsm = 0; a.eps = L.eps; a.N = L.N; a.M = L.M; a.Mp = L.Mp;
-  a.part = nullptr; a.groups = 0; a.rslot_in = nullptr; a.win = WinCoef{0.f, 0.f, 0.f}; a.nstar = nullptr;
+  a.part = nullptr; a.groups = 0; a.candcap = 0; a.rslot_in = nullptr; a.win = WinCoef{0.f, 0.f, 0.f}; a.nstar = nullptr;
   a.cstar = nullptr;
   a.At = L.At; a.inv_norm = L.inv_norm; a.G = L.G; a.ldg = L.ldg;
   a.Y = L.Y; a.ldy = L.ldy; a.F = L.F; a.ldf = L.ldf; a.U = L.U; a.ldu = L.ldu; a.X = L.X; a.ldx = L.ldx;

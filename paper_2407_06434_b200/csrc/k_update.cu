@@ -45,7 +45,8 @@ namespace ompb {
 #ifndef OMP_RF_CAP
 #define OMP_RF_CAP 512
 #endif
-constexpr int RF_CAP = OMP_RF_CAP;   // explicit candidate list capacity (beyond: all N atoms)
+constexpr int RF_CAP = OMP_RF_CAP;   // largest kept-entry list (beyond: all N atoms); a launch sizes its list
+                                     // min(RF_CAP, groups x TOPK), so it overflows only when N > 16 384
 constexpr int GRP_CAP = 64;          // overflowing 128-atom groups re-evaluated whole (beyond: all N)
 constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared memory
 // columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
@@ -88,8 +89,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update):
   //   [the fp32 residual row (refine): Mp floats; else Mp / 4 floats] [w, z, u, xs: Sp floats each]
-  //   [ss, ro: Sp ints each] [cand: RF_CAP ints (refine)] [F_k packed (fsm)]
-  //   [cand: RF_CAP ints (refine)]
+  //   [ss, ro: Sp ints each] [cand: a.candcap ints (refine)] [F_k packed (fsm)]
   extern __shared__ __align__(16) uint8_t dsm[];
   float4* rsm = reinterpret_cast<float4*>(dsm);
   // (the first region doubles as the tail's ||r||^2 chunk partials, Mp / 4 floats, after the refine)
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   // a small packed F_k (fsm: decided at launch) goes to shared memory too: the column dots z = F^T w
   // and the row sweeps F z, F u then read shared memory instead of dependent L2 round trips
-  float* Fs = reinterpret_cast<float*>(cand + (REFINE ? RF_CAP : 0));
+  float* Fs = reinterpret_cast<float*>(cand + (REFINE ? a.candcap : 0));
   if constexpr (FSM) {
     const int f4 = (k * (k + 1) / 2 + 3) >> 2;          // within the row: ldf >= S(S+1)/2 rounded to 4
     const float4* fg = reinterpret_cast<const float4*>(a.F + b * a.ldf);
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
           const int n = __float_as_int(p.y);
           if (p.x >= thr && n >= 0 && n < a.N) {
             const int at = atomicAdd(&ncand, 1);
-            if (at >= RF_CAP) full = true;
+            if (at >= a.candcap) full = true;
             else cand[at] = n;
           }
         }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     UPD_TRACE(1);
 #ifdef OMP_UPDATE_TRACE
     if (tid == 0 && a.k == g_upd_trace_k) {   // candidate statistics: sum, > 16, > 128, full fallback
-      const int nc = min(ncand, RF_CAP) + min(ngrp, GRP_CAP) * SCREEN_GROUP;
+      const int nc = min(ncand, a.candcap) + min(ngrp, GRP_CAP) * SCREEN_GROUP;
       atomicAdd(&g_upd_clk[12], (unsigned long long)nc);
       if (nc > 16) atomicAdd(&g_upd_clk[13], 1ull);
       if (ngrp > 0) atomicAdd(&g_upd_clk[14], 1ull);
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     bool nan_c = false;
     // the kept entries, then every atom of each overflowing group (no atom is in both); more than the
     // lists hold: all N atoms
-    const int nind = min(ncand, RF_CAP), ng = min(ngrp, GRP_CAP);
+    const int nind = min(ncand, a.candcap), ng = min(ngrp, GRP_CAP);
     const int count = full ? (int)a.N : nind + ng * SCREEN_GROUP;
     for (int j = warp; j < count; j += T / 32) {
       int n;
@@ -395,7 +395,9 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
 #define OMP_FSM_MP_MAX 1024
 #endif
   a.fsm = (refine && fk * 4 <= kFsmMaxBytes && (L.B < 8192 || L.Mp <= OMP_FSM_MP_MAX)) ? 1 : 0;
-  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (refine ? RF_CAP * 4 : 0) +
+  // the kept entries of one signal are at most groups x TOPK: a list that size never overflows
+  a.candcap = refine ? (int)min((int64_t)RF_CAP, (int64_t)L.groups * TOPK) : 0;
+  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (size_t)a.candcap * 4 +
                       (a.fsm ? (size_t)fk * 4 : 0);
   if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)
                            : launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);

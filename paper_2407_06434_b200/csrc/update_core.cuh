@@ -39,6 +39,7 @@ struct UpdateArgs {
   // selection inputs
   const float2* part;   // screen partials (REFINE)
   int groups;           // screen partial groups per row (Np / SCREEN_GROUP)
+  int candcap;          // capacity of the refine's kept-entry list (k_update)
   const float* rslot_in;  // window W of each row of the current buffer (REFINE)
   WinCoef win;          // coefficients of the next window (written to rslot_out)
   const int32_t* nstar; // preselected (SIMT mode)
