@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
 #endif
   // (no L2 prefetch of y: measured at c4, its lines are evicted before the residual phase reads them
-  // -- 0.84 GB of extra DRAM reads per launch for 0.8 GB of y, and 1.2 % slower; profiles/r02/ab_dram)
+  // -- 0.84 GB of extra DRAM reads per launch for 0.8 GB of y, and 1.2 % slower; profiles/r02/ab_dram;
+  // nor a shared-memory copy: 8 % slower at c4, 3 % at c5 -- the L1 it takes from the F_k prefetch --
+  // for 1 % at c2 / c3, profiles/r02/ab/ab_ystage_r02g.txt.  The gather's accumulator starts at y.)
 
   // ---- a3: selection ------------------------------------------------------------------------------
   if constexpr (REFINE) {
@@ -284,11 +286,12 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, kZC, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr, &upd_t0_);
+  append_residual<T, CH, P, kZC, SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
+                                                        &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
 #else
-  append_residual<T, CH, P, kZC, SEL == SEL_PROJ>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, kZC, SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 

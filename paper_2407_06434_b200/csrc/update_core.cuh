@@ -228,7 +228,9 @@ struct TailSmem {
 // rows_sm (nullable): a shared-memory copy of the support's atom rows (row j at rows_sm + j q4,
 // j <= k; row k may still be landing by cp.async, waited for here) that the gather reads instead
 // of A^T in global memory -- the same values, so the same result.
-template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false>
+// FZ8: the row sweep keeps 8 column loads in flight (F_k in L1 / L2); with F_k in shared memory 4 do,
+// and the smaller code keeps more of the kernel in the instruction cache (same FMA order either way).
+template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false, bool FZ8 = true>
 __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
                                                 const float cst, const TailSmem& sm, const float* Fb,
                                                 float* Fs_append, const float4* rows_sm = nullptr,
@@ -336,7 +338,7 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     int j = i & ~31;
     int o = j * (j + 1) / 2 + i;                  // offset of F[i, j] in the packed columns
     // 8 column loads in flight (F_k of a large S lives in L2, not L1), the FMAs in the same order
-    for (; j + 8 <= k; j += 8) {
+    if constexpr (FZ8) for (; j + 8 <= k; j += 8) {
       float f[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -402,20 +404,54 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   OMP_TAIL_TRACE(3);
 
   // ---- a5: residual r = y - A_S x, ||r||, eps test, next screening operand ------------------------
-  // L2-bandwidth bound gather: per atom pair, every thread issues its 2 x CH float4 loads before the
-  // FMAs; with T * CH == Mp / 4 (the benchmark shapes) no load is predicated.
+  // L2-bandwidth bound gather: per group of P rows, every thread issues its P x CH float4 loads before
+  // the FMAs (with T * CH == Mp / 4, the benchmark shapes, no load is predicated off).
   const int kk = k + 1;
   const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+  // r = y - sum_j x_j a_{s_j}, in one of two orders fixed by the row width (so every kernel and block
+  // size computes a signal the same way):
+  //   Mp <= 1024: acc starts at y and takes fmaf(-x_j, a_j, acc), j ascending -- y's loads go out with
+  //     the first rows', no round trip of their own after the gather (c5: +5 %, c2 / c3: +1 %);
+  //   wider rows: acc = sum_j x_j a_j, j ascending, then r = y - acc (y loaded after the gather: holding
+  //     it through the gather costs the wide-row kernels registers, c4: -3 %; profiles/r02/ab)
+  // A compile-time choice: both kernels' (T, CH) maps give T x CH = the power of two >= Mp / 4 (>= 32),
+  // so T x CH <= 256 <=> Mp <= 1024 in k_update and k_small alike.
+  constexpr bool yfirst = T * CH <= 256;
+  const float* y = a.Y + b * a.ldy;
+  const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
+  auto load_y = [&](int c) {
+    const int q = tid + c * T;
+    const int64_t m = (int64_t)q << 2;
+    float4 v;
+    if (yvec && m + 3 < a.M) {
+      v = ldg_policy(reinterpret_cast<const float4*>(y + m), stream);
+    } else {
+      v.x = m < a.M ? y[m] : 0.f;
+      v.y = m + 1 < a.M ? y[m + 1] : 0.f;
+      v.z = m + 2 < a.M ? y[m + 2] : 0.f;
+      v.w = m + 3 < a.M ? y[m + 3] : 0.f;
+    }
+    return v;
+  };
   float4 acc[CH];
+  {
 #pragma unroll
-  for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < CH; ++c) {
+      const int q = tid + c * T;
+      if (q >= q4 || !yfirst) {
+        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        acc[c] = load_y(c);
+      }
+    }
+  }
   const float4* A4 = reinterpret_cast<const float4*>(a.At) + tid;
   {
     // chunk c of this thread exists for every row (T * CH == q4 at the benchmark shapes: no predicate)
     bool has[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) has[c] = (T * CH == q4) || (tid + c * T < q4);
-    // fold x_j times row j into acc, j ascending; rows come P at a time (loads before FMAs)
+    // fold (-)x_j times row j into acc, j ascending; rows come P at a time (loads before FMAs)
     const bool full = (T * CH == q4);
     auto fold = [&](const float x, const float4 (&v)[CH]) {
 #pragma unroll
@@ -435,12 +471,12 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
 #pragma unroll
         for (int p = 0; p < P; ++p) load_row(j + p, v[p]);
 #pragma unroll
-        for (int p = 0; p < P; ++p) fold(xs[j + p], v[p]);
+        for (int p = 0; p < P; ++p) fold(yfirst ? -xs[j + p] : xs[j + p], v[p]);
       }
       for (; j < kk; ++j) {
         float4 v[CH];
         load_row(j, v);
-        fold(xs[j], v);
+        fold(yfirst ? -xs[j] : xs[j], v);
       }
     };
     if (rows_sm) {
@@ -449,7 +485,8 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
 #pragma unroll
         for (int c = 0; c < CH; ++c) v[c] = has[c] ? r[c * T] : make_float4(0.f, 0.f, 0.f, 0.f);
       });
-    } else if (full) {           // every chunk exists: unpredicated loads
+    } else if (full) {           // every chunk exists: unpredicated loads (measured: the predicated form
+                                 // alone doubled the c4 update's time)
       gather([&](int j, float4 (&v)[CH]) {
         const float4* r = A4 + ro[j];
 #pragma unroll
@@ -464,23 +501,15 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     }
   }
   OMP_TAIL_TRACE(4);
-  const float* y = a.Y + b * a.ldy;
-  const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int q = tid + c * T;
     if (q < q4) {
-      const int64_t m = (int64_t)q << 2;
-      float4 yv;
-      if (yvec && m + 3 < a.M) {
-        yv = ldg_policy(reinterpret_cast<const float4*>(y + m), stream);
-      } else {
-        yv.x = m < a.M ? y[m] : 0.f;
-        yv.y = m + 1 < a.M ? y[m + 1] : 0.f;
-        yv.z = m + 2 < a.M ? y[m + 2] : 0.f;
-        yv.w = m + 3 < a.M ? y[m + 3] : 0.f;
+      if (!yfirst) {
+        const float4 yv = load_y(c);
+        acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);
       }
-      acc[c] = make_float4(yv.x - acc[c].x, yv.y - acc[c].y, yv.z - acc[c].z, yv.w - acc[c].w);   // r
+      // acc[c] = r
       // ||r||^2: one partial per float4 chunk, summed below in an order that does not depend on T
       if constexpr (!V0) {
         sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));

@@ -1,0 +1,27 @@
+#!/bin/bash
+# A/B of an environment switch on a set of bench configs (graph path), alternating A and B runs on one box:
+#   bash scripts/ab_env.sh TAG VAR VALUE_A VALUE_B "bench args 1" "bench args 2" ...
+set -u
+TAG=$1; VAR=$2; VA=$3; VB=$4; shift 4
+OUT=gpurun_out/ab_${TAG}.txt
+mkdir -p gpurun_out
+for args in "$@"; do
+  for rep in 1 2; do
+    for v in $VA $VB; do
+      line=$(env $VAR=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-kernel-profile $args 2>/dev/null | tail -1)
+      python - "$v" "$args" "$line" >> $OUT <<'PY'
+import json, sys
+v, args, line = sys.argv[1:4]
+try:
+    d = json.loads(line)
+    k = d.get("kernels", {})
+    upd = k.get("update", {})
+    cor = k.get("correlation", {})
+    print(f"{args:45s} {v:>4s}  {d['value']:14,.0f} signals/s  {d['ms_per_step']:9.3f} ms/step  update {upd.get('ms_total', 0) / max(1, upd.get('launches', 1)):.4f} ms  corr {cor.get('ms_total', 0) / max(1, cor.get('launches', 1)):.4f} ms  clk {d['clocks'].get('sm_mhz')}")
+except Exception as e:
+    print(f"{args:45s} {v:>4s}  FAILED {e}")
+PY
+    done
+  done
+done
+cat $OUT
