@@ -474,7 +474,7 @@ def main():
                        "path": path,
                        "parallelism": f"batch-shard x{world}",
                        "collectives": ("none" if world == 1 else
-                                       "NCCL: A broadcast once (setup); per step scatter Y from rank 0, "
+                                       f"{args.dist_backend.upper()}: A broadcast once (setup); per step scatter Y from rank 0, "
                                        "gather the packed results to rank 0 (inside the timed span)")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "kernels": kernels,
