@@ -337,10 +337,17 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// (T, CH) for the row width; "few" = at most 2 CTAs per SM in the whole launch
+// (T, CH) for the row width; "few" = at most 2 CTAs per SM in the whole launch; "mid" = the whole launch
+// resident at once with at most 8 CTAs per SM: the per-signal chain sets the launch time, so each thread
+// keeps 8 float4 chunks (8 / CH rows) in flight in the gather instead of 2 rows.  Measured (graph path,
+// profiles/r02/ab/ab_mid_r02m.txt): c2 +2.8 %, M = 1024 at B = 10^3 +2.7 %, t2m1024 at B = 10^3 +6.6 %,
+// but c5 at B = 10^3 (T = 128, CH = 1) -1.2 %, which therefore keeps 2.  OMP_B200_MID=0: off (A/B)
 template <int SEL, int T, int CH>
-static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, bool few, cudaStream_t st) {
+static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, bool few, bool mid,
+                             cudaStream_t st) {
   if (few) return launch_t<SEL, T, CH, 1, (16 / CH > 2 ? 16 / CH : 2)>(a, B, smem, persist, st);
+  if constexpr ((T <= 64 && CH <= 2) || (T == 128 && CH == 2))
+    if (mid) return launch_t<SEL, T, CH, 8, (8 / CH > 2 ? 8 / CH : 2)>(a, B, smem, persist, st);
   constexpr int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32);
   return launch_t<SEL, T, CH, MINB, (OMP_UPDATE_PCH / CH > 2 ? OMP_UPDATE_PCH / CH : 2)>(a, B, smem, persist, st);
 }
@@ -358,6 +365,12 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
       sms = 148;
   }
   const bool few = B <= 2 * (int64_t)sms;
+  static int mid_env = -1;
+  if (mid_env < 0) {
+    const char* e = getenv("OMP_B200_MID");
+    mid_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool mid = mid_env && B <= 8 * (int64_t)sms;
   const int64_t q4 = a.Mp / 4;
   // Large batches of narrow rows (many waves: throughput) take one warp per signal and 32 signals per
   // SM; smaller batches keep the wider CTAs, whose shorter per-signal chain sets the launch time when
@@ -365,15 +378,15 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
   // +24 % at 10^5, but -24 % at B = 10^3 and -30 % at 100; c3 (M = 1024, B = 10^4, eps stops): T = 64
   // vs 128 -11 % -- hence only M <= 512 and B >= 8192.
   const bool wide_batch = B >= 8192;
-  if (q4 <= 32) return launch_tc<SEL, 32, 1>(a, B, smem, persist, few, st);
-  if (q4 <= 64) return wide_batch ? launch_tc<SEL, 32, 2>(a, B, smem, persist, few, st)
-                                  : launch_tc<SEL, 64, 1>(a, B, smem, persist, few, st);
-  if (q4 <= 128) return wide_batch ? launch_tc<SEL, 32, 4>(a, B, smem, persist, few, st)
-                                   : launch_tc<SEL, 128, 1>(a, B, smem, persist, few, st);
-  if (q4 <= 256) return launch_tc<SEL, 128, 2>(a, B, smem, persist, few, st);
-  if (q4 <= 512) return launch_tc<SEL, 128, 4>(a, B, smem, persist, few, st);
-  if (q4 <= 1024) return launch_tc<SEL, 256, 4>(a, B, smem, persist, few, st);
-  if (q4 <= 2048) return launch_tc<SEL, 256, 8>(a, B, smem, persist, few, st);
+  if (q4 <= 32) return launch_tc<SEL, 32, 1>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 64) return wide_batch ? launch_tc<SEL, 32, 2>(a, B, smem, persist, few, mid, st)
+                                  : launch_tc<SEL, 64, 1>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 128) return wide_batch ? launch_tc<SEL, 32, 4>(a, B, smem, persist, few, mid, st)
+                                   : launch_tc<SEL, 128, 1>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 256) return launch_tc<SEL, 128, 2>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 512) return launch_tc<SEL, 128, 4>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 1024) return launch_tc<SEL, 256, 4>(a, B, smem, persist, few, mid, st);
+  if (q4 <= 2048) return launch_tc<SEL, 256, 8>(a, B, smem, persist, few, mid, st);
   return cudaErrorNotSupported;   // M > 8192
 }
 

@@ -21,9 +21,32 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "omp_internal.cuh"
 
 using namespace ompb;
+
+// NVTX ranges (domain "omp_b200") around the ABI calls, the graph capture and each enqueued iteration,
+// for nsys / ncu range filtering (SURVEY §5 "Tracing / profiling").  Header-only NVTX 3: without an
+// attached tool every push / pop is a no-op.
+namespace {
+nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("omp_b200");
+  return d;
+}
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t at = {};
+    at.version = NVTX_VERSION;
+    at.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    at.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    at.message.ascii = name;
+    nvtxDomainRangePushEx(nvtx_domain(), &at);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
+}  // namespace
 
 struct ProfRec {
   int slot;
@@ -514,6 +537,7 @@ static ompStatus_t enqueue_screened(ompHandle_t h, const WsView& w, const float*
   if (e != cudaSuccess) return cuda_fail(h, e);
   const Operand At = atoms_operand(h);
   for (int32_t k = 0; k < S; ++k) {
+    NvtxRange nv_it("omp iteration (screen + update)");
     const int cur = k & 1, nxt = cur ^ 1;
     const Operand R = view_operand(h, w, B, cur);
     if (tc_mode(h)) {
@@ -691,6 +715,7 @@ static ompStatus_t run_batch(ompHandle_t h, const float* Y, int64_t B, int64_t l
     if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
       return cuda_fail(h, cudaGetLastError());
     // capture only records the launches; the replay is ordered on the caller's stream
+    NvtxRange nv_cap("ompBatch: capture CUDA graph");
     cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_fail(h, e);
     std::vector<ProfRec> prof;
@@ -834,6 +859,7 @@ ompStatus_t ompCreate(ompHandle_t* out, int device, const float* A, int64_t M, i
     cudaGetLastError();
     return OMP_ERR_INVALID_ARG;
   }
+  NvtxRange nv("ompCreate (setup: validate, norms, planes, Gram)");
   DevGuard g(device);
   cudaStream_t st = (cudaStream_t)stream;
   ompHandle_t h = new (std::nothrow) ompHandle_st();
@@ -930,6 +956,7 @@ ompStatus_t ompBatch(ompHandle_t h, const float* Y, int64_t B, int64_t ldy, int3
   ompStatus_t s = check_batch_args(h, Y, B, ldy, S, X, ldx, support, lds, resid, n_iter, status);
   if (s != OMP_OK) return s;
   if (B == 0) return OMP_OK;
+  NvtxRange nv("ompBatch");
   DevGuard g(h->device);
   return run_batch(h, Y, B, ldy, S, eps, X, ldx, support, lds, resid, n_iter, status,
                    (cudaStream_t)stream);
@@ -941,6 +968,7 @@ ompStatus_t ompBatchHost(ompHandle_t h, const float* Yh, int64_t B, int64_t ldy,
   ompStatus_t s = check_batch_args(h, Yh, B, ldy, S, Xh, ldx, suph, lds, resh, nith, sth);
   if (s != OMP_OK) return s;
   if (B == 0) return OMP_OK;
+  NvtxRange nv("ompBatchHost");
   DevGuard g(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   if (B > h->capHB || S > h->capHS) {
