@@ -190,11 +190,11 @@ def kernel_work(cfg, B, mode, path="residual", n_iter=None):
             "update": ("l2", hbm + l2, "GB/s", {"hbm_bytes": hbm, "l2_gather_bytes": l2}),
             "init": ("hbm", B * 4.0 * (2 * M + Mp), "GB/s", None),
         }
-    tiles = math.ceil(N / 256)
+    groups = 2 * math.ceil(N / 256)                # 128-atom screen groups (Np / 128)
     planes = {"bf16": 2.0, "3xtf32": 8.0, "simt": 0.0}[mode]
     # update = exact selection + factor append + residual, split into streamed (HBM) and gathered (L2)
     hbm = per_launch(4.0 * Mp                      # fp32 residual row read by the selection
-                     + 8.0 * 4 * tiles             # screen partials
+                     + 8.0 * 4 * groups            # screen partials: TOPK = 4 float2 per group
                      + 4.0 * ks * (ks + 1) / 2     # packed F_k staged once
                      + 4.0 * (ks + 2) * 3          # new F column, x, u
                      + 4.0 * M                     # y

@@ -48,3 +48,16 @@ def test_update_bytes_split():
     assert total == pytest.approx(split["hbm_bytes"] + split["l2_gather_bytes"])
     ks = np.arange(S)
     assert split["l2_gather_bytes"] == pytest.approx(float((4.0 * M * (ks + 2)).sum() / S))
+
+
+def test_update_streamed_bytes_count_every_screen_partial():
+    """The screen writes TOPK = 4 (value, index) float2 per 128-atom group (Np / 128 groups), and the update
+    reads all of them: 8 x 4 x Np / 128 bytes per signal-iteration (round 1 counted per 256-atom tile)."""
+    cfg = config("c4")
+    S, M, N = cfg["S"], cfg["M"], cfg["N"]
+    Mp = -(-M // 64) * 64
+    ks = np.arange(S, dtype=np.float64)
+    hbm = bench.kernel_work(cfg, 1, "bf16", "residual")["update"][3]["hbm_bytes"]
+    want = (4.0 * Mp + 8.0 * 4 * (N // 128) + 4.0 * ks * (ks + 1) / 2 + 4.0 * (ks + 2) * 3 + 4.0 * M
+            + (4.0 + 2.0) * Mp).sum() / S
+    assert hbm == pytest.approx(want)
