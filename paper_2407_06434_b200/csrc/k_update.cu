@@ -26,6 +26,15 @@
 // thread 0, summed over every CTA of the launch at iteration g_upd_trace_k
 __device__ int g_upd_trace_k = -1;
 __device__ unsigned long long g_upd_clk[16];
+// the SM clock inside the traced launch: (clock64, globaltimer) of the first and the last CTA at their
+// start and end (each pair measures its own SM over the CTA's lifetime)
+__device__ unsigned long long g_upd_freq[8];
+__device__ __forceinline__ void upd_freq_mark(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  g_upd_freq[2 * slot] = clock64();
+  g_upd_freq[2 * slot + 1] = t;
+}
 #define UPD_TRACE(p)                                                                   \
   do {                                                                                 \
     if (threadIdx.x == 0 && a.k == g_upd_trace_k) {                                    \
@@ -79,6 +88,10 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   // PDL (screened path): wait for the screen's completion, then let the next screen launch early
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef OMP_UPDATE_TRACE
+  const bool freq_cta = threadIdx.x == 0 && a.k == g_upd_trace_k && (b == 0 || b == gridDim.x - 1);
+  if (freq_cta) upd_freq_mark(b == 0 ? 0 : 2);
+#endif
   if (a.status[b] != SIG_RUNNING) return;
 #ifdef OMP_UPDATE_TRACE
   unsigned long long upd_t0_ = clock64();
@@ -290,6 +303,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
                                                         &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
+  if (freq_cta) upd_freq_mark(b == 0 ? 1 : 3);
 #else
   append_residual<T, CH, P, kZC, SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
@@ -433,5 +447,9 @@ extern "C" int omp_debug_update_trace(int k, unsigned long long* host16) {
     return (int)e;
   }
   return (int)cudaMemcpyFromSymbol(host16, g_upd_clk, sizeof(unsigned long long) * 16);
+}
+
+extern "C" int omp_debug_update_freq(unsigned long long* host8) {
+  return (int)cudaMemcpyFromSymbol(host8, g_upd_freq, sizeof(unsigned long long) * 8);
 }
 #endif

@@ -60,6 +60,12 @@ def main():
             print(f"   {name:20s} {v[p] / n:9.0f}  {100 * v[p] / n / tot:5.1f} %")
         print(f"   candidates: mean {v[12] / n:.2f}, > 16: {int(v[13])}, with an overflowing group: {int(v[14])}, "
               f"all-N fallback: {int(v[3])} of {int(n)} signals")
+        fq = (ctypes.c_ulonglong * 8)()
+        lib.omp_debug_update_freq.argtypes = [ctypes.c_void_p]
+        lib.omp_debug_update_freq(fq)
+        f = np.array(fq, dtype=np.float64)
+        mhz = [1e3 * (f[2 * e] - f[2 * s]) / max(1.0, f[2 * e + 1] - f[2 * s + 1]) for s, e in ((0, 1), (2, 3))]
+        print(f"   SM clock inside the launch: first CTA {mhz[0]:.0f} MHz, last CTA {mhz[1]:.0f} MHz")
 
 
 if __name__ == "__main__":
