@@ -61,6 +61,13 @@ constexpr int64_t kFsmMaxBytes = 8192;   // largest packed F_k staged in shared 
 // columns per warp in z = F^T w (interleaving only: no column's arithmetic changes; measured: 4 or 8
 // cost registers and lose at c4 and at c5 B = 10^5)
 constexpr int kZC = 2;
+// one-warp CTAs (T = 32) take OMP_ZC32 columns per round: their single warp walks all k columns, so more
+// of them in flight hides more of the shuffle trees' latency (same arithmetic per column).  Measured
+// (profiles/r02/ab/ab_zc_r02o.txt): 4 columns vs 2, c5 B = 10^5 +3.2 %, B = 10^4 +4.4 %; 3: +1.3 / +2.3 %;
+// round 1: 8 lost (spills)
+#ifndef OMP_ZC32
+#define OMP_ZC32 4
+#endif
 
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
@@ -299,13 +306,13 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, kZC, SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
+  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
                                                         &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
   if (freq_cta) upd_freq_mark(b == 0 ? 1 : 3);
 #else
-  append_residual<T, CH, P, kZC, SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 

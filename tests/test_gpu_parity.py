@@ -597,3 +597,40 @@ def test_projection_needs_n_at_most_8192():
         out = dict(support=r.support.cpu().numpy(), X=r.X.cpu().numpy(), resid=r.resid_norm.cpu().numpy(),
                    n_iter=r.n_iter.cpu().numpy(), status=r.status.cpu().numpy())
     assert_no_bugs(parity(out, A, Y, S, None, range(4)), "N=9000 residual")
+
+
+def test_persisting_l2_limit_is_restored():
+    """ompCreate raises the device's persisting-L2 limit for the atom table (process state); the last
+    handle on the device to be destroyed restores the caller's value (and a second handle in between
+    keeps it raised)."""
+    import ctypes
+    import torch
+    from paper_2407_06434_b200 import OMP
+    torch.cuda.init()
+    rt = None
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            rt = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    if rt is None:
+        pytest.skip("libcudart not loadable")
+    LIMIT_PERSISTING_L2 = 0x06            # cudaLimitPersistingL2CacheSize
+
+    def limit():
+        v = ctypes.c_size_t()
+        assert rt.cudaDeviceGetLimit(ctypes.byref(v), LIMIT_PERSISTING_L2) == 0
+        return v.value
+
+    assert rt.cudaDeviceSetLimit(LIMIT_PERSISTING_L2, ctypes.c_size_t(0)) == 0
+    before = limit()
+    A = torch.from_numpy(make_dictionary(2048, 4096, 3)).cuda()
+    h1 = OMP(A)
+    raised = limit()
+    h2 = OMP(A)
+    h1.close()
+    assert limit() == raised              # h2 still holds it
+    h2.close()
+    assert limit() == before
+    assert raised > before
