@@ -234,18 +234,40 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     // lists hold: all N atoms
     const int nind = min(ncand, a.candcap), ng = min(ngrp, GRP_CAP);
     const int count = full ? (int)a.N : nind + ng * SCREEN_GROUP;
-    for (int j = warp; j < count; j += T / 32) {
-      int n;
-      if (full) n = j;
-      else if (j < nind) n = cand[j];
-      else {
-        n = grp[(j - nind) / SCREEN_GROUP] * SCREEN_GROUP + (j - nind) % SCREEN_GROUP;
-        if (n >= a.N) continue;                        // the last group's padding (warp-uniform)
-      }
-      const float c = warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane);
+    // candidate j of the list (-1 past the end or on the last group's padding)
+    auto cand_at = [&](int j) -> int {
+      if (j >= count) return -1;
+      if (full) return j;
+      if (j < nind) return cand[j];
+      const int n = grp[(j - nind) / SCREEN_GROUP] * SCREEN_GROUP + (j - nind) % SCREEN_GROUP;
+      return n < a.N ? n : -1;
+    };
+    auto consider = [&](int n, float c) {
       nan_c |= isnan(c);
       const Cand cd{fabsf(c) * a.inv_norm[n], n, c};
       if (cand_better(cd, best)) best = cd;
+    };
+    // rows of <= 1024 floats: two candidates per warp at a time, their row loads in flight together (each
+    // dot in warp_dot's order; the best is order-independent).  Measured (profiles/r02/ab/ab_dot2_r02q.txt):
+    // c3 +1.5 %, c2 / c5 +-0; at c4 (8 KB rows) -1 %, so wider rows keep one at a time.
+    constexpr int NWR = T / 32;
+    constexpr int PAIR = (T * CH <= 256) ? 2 : 1;
+    for (int j = warp; j < count; j += PAIR * NWR) {
+      if constexpr (PAIR == 1) {
+        const int n = cand_at(j);
+        if (n >= 0) consider(n, warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
+        continue;
+      }
+      const int n1 = cand_at(j), n2 = cand_at(j + NWR);
+      if (n1 >= 0 && n2 >= 0) {
+        const float2 c = warp_dot2(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n1 * a.Mp),
+                                   reinterpret_cast<const float4*>(a.At + (int64_t)n2 * a.Mp), q4, lane);
+        consider(n1, c.x);
+        consider(n2, c.y);
+      } else if (n1 >= 0 || n2 >= 0) {
+        const int n = n1 >= 0 ? n1 : n2;
+        consider(n, warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
+      }
     }
     if (lane == 0) red_c[warp] = best;
     const int any_nan = __syncthreads_or(nan_c);      // residual row no longer needed past here
@@ -370,7 +392,11 @@ static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t
   if constexpr ((T <= 64 && CH <= 2) || (T == 128 && CH == 2))
     if (mid) return launch_t<SEL, T, CH, 8, (8 / CH > 2 ? 8 / CH : 2)>(a, B, smem, persist, st);
   constexpr int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32);
-  return launch_t<SEL, T, CH, MINB, (OMP_UPDATE_PCH / CH > 2 ? OMP_UPDATE_PCH / CH : 2)>(a, B, smem, persist, st);
+#ifndef OMP_P32
+#define OMP_P32 2
+#endif
+  constexpr int P = (T == 32 && CH == 4) ? OMP_P32 : (OMP_UPDATE_PCH / CH > 2 ? OMP_UPDATE_PCH / CH : 2);
+  return launch_t<SEL, T, CH, MINB, P>(a, B, smem, persist, st);
 }
 
 template <int SEL>

@@ -176,6 +176,39 @@ __device__ __forceinline__ float warp_dot(const float4* __restrict__ r4, const f
   return acc;
 }
 
+// two such dots (rows a4, b4 against the same r4) with their loads in flight together; each result is
+// bit for bit warp_dot's
+__device__ __forceinline__ float2 warp_dot2(const float4* __restrict__ r4, const float4* __restrict__ a4,
+                                           const float4* __restrict__ b4, int q4, int lane) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+  int q = lane;
+  for (; q + 96 < q4; q += 128) {
+    const float4 a0 = __ldg(a4 + q), a1 = __ldg(a4 + q + 32), a2 = __ldg(a4 + q + 64), a3 = __ldg(a4 + q + 96);
+    const float4 b0 = __ldg(b4 + q), b1 = __ldg(b4 + q + 32), b2 = __ldg(b4 + q + 64), b3 = __ldg(b4 + q + 96);
+    const float4 r0 = r4[q], r1 = r4[q + 32], r2 = r4[q + 64], r3 = r4[q + 96];
+    s0 = fma4(r0, a0, s0);
+    s1 = fma4(r1, a1, s1);
+    s2 = fma4(r2, a2, s2);
+    s3 = fma4(r3, a3, s3);
+    t0 = fma4(r0, b0, t0);
+    t1 = fma4(r1, b1, t1);
+    t2 = fma4(r2, b2, t2);
+    t3 = fma4(r3, b3, t3);
+  }
+  for (; q < q4; q += 32) {
+    const float4 r = r4[q];
+    s0 = fma4(r, __ldg(a4 + q), s0);
+    t0 = fma4(r, __ldg(b4 + q), t0);
+  }
+  float x = (s0 + s1) + (s2 + s3), y = (t0 + t1) + (t2 + t3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+    y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
+  return make_float2(x, y);
+}
+
 // the same dot with the atom's chunks held in registers (areg[i] = chunk lane + 32 i, KC >= chunks)
 template <int KC>
 __device__ __forceinline__ float warp_dot_regs(const float4* __restrict__ r4, const float4 (&areg)[KC], int q4,
