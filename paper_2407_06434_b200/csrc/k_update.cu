@@ -68,6 +68,12 @@ constexpr int kZC = 2;
 #ifndef OMP_ZC32
 #define OMP_ZC32 4
 #endif
+// with F_k in shared memory, CTAs of <= OMP_ZLANE_TMAX threads sum z = F^T w thread per column (the same
+// bits; update_core.cuh).  Measured (profiles/r02/ab/ab_zlane_r02r.txt): c5 B = 10^5 / 10^4 (T = 32)
+// +4 / +3.7 %, c2 (T = 64) +5.7 %; T = 128 lost (c3 -2.7 %, c5 B = 10^3 -3 %: register spills)
+#ifndef OMP_ZLANE_TMAX
+#define OMP_ZLANE_TMAX 64
+#endif
 
 // SEL: how n* is found -- SEL_GIVEN (nstar/cstar from k_select), SEL_SCREEN (refine the screen's
 // candidates), SEL_PROJ (projection path: exact argmax over the projection row p = A^T r_k)
@@ -87,6 +93,17 @@ constexpr int SEL_SCREEN_FSM = 3;   // SEL_SCREEN with the packed F_k staged in 
 #ifndef OMP_UPDATE_PCH
 #define OMP_UPDATE_PCH 2
 #endif
+// bytes of the first dynamic shared-memory region: the staged fp32 residual row (refine: Mp floats; it
+// doubles as the tail's ||r||^2 chunk partials), or just those partials (Mp / 4 floats); none for one-warp
+// CTAs, which sum ||r||^2 in registers (append_residual) and read the row from global memory
+#ifndef OMP_RG
+#define OMP_RG 1
+#endif
+template <int T>
+__host__ __device__ constexpr size_t update_region0(bool refine, int64_t Mp) {
+  return (T == 32 && OMP_RG) ? 0 : (refine ? (size_t)Mp * 4 : (size_t)Mp);
+}
+
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool REFINE = (SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM);
@@ -107,13 +124,18 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
   const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
-  // dynamic shared memory (sizes in launch_update):
-  //   [the fp32 residual row (refine): Mp floats; else Mp / 4 floats] [w, z, u, xs: Sp floats each]
+  // dynamic shared memory (sizes in launch_update / launch_t):
+  //   [update_region0: the fp32 residual row (refine): Mp floats; else Mp / 4 floats; one-warp CTAs: none]
+  //   [w, z, u, xs: Sp floats each]
   //   [ss, ro: Sp ints each] [cand: a.candcap ints (refine)] [F_k packed (fsm)]
   extern __shared__ __align__(16) uint8_t dsm[];
+  // one-warp CTAs (RG) keep no residual row in shared memory: the refine reads it from global memory
+  // (prefetched into L1 at the start) and the tail sums ||r||^2 in registers, so the 32 CTAs per SM
+  // also fit at the last iterations of c5 (with the row staged, k >= 37 left 23..31)
+  constexpr bool RG = (T == 32) && OMP_RG;
   float4* rsm = reinterpret_cast<float4*>(dsm);
   // (the first region doubles as the tail's ||r||^2 chunk partials, Mp / 4 floats, after the refine)
-  float* w = reinterpret_cast<float*>(dsm + (REFINE ? (size_t)a.Mp * 4 : (size_t)a.Mp));
+  float* w = reinterpret_cast<float*>(dsm + update_region0<T>(REFINE, a.Mp));
   float* z = w + Sp;
   float* u = z + Sp;
   float* xs = u + Sp;
@@ -140,10 +162,14 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     cp_async4(&ss[j], a.support + b * a.lds + j);
     cp_async4(&u[j], a.U + b * a.ldu + j);
   }
-  if constexpr (REFINE) {
-    const float4* r4g = reinterpret_cast<const float4*>(a.R32in + (int64_t)cur_slot * a.Mp);
+  const float4* r4g = reinterpret_cast<const float4*>(a.R32in + (int64_t)cur_slot * a.Mp);
+  if constexpr (REFINE && !RG) {
     for (int q = tid; q < q4; q += T) cp_async16(&rsm[q], r4g + q);
+  } else if constexpr (REFINE) {
+    for (uint32_t o = (uint32_t)tid * 128u; o < (uint32_t)a.Mp * 4u; o += (uint32_t)T * 128u)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(r4g) + o));
   }
+  const float4* rrow = RG ? r4g : rsm;   // the residual row the refine's dots read
   // a small packed F_k (fsm: decided at launch) goes to shared memory too: the column dots z = F^T w
   // and the row sweeps F z, F u then read shared memory instead of dependent L2 round trips
   float* Fs = reinterpret_cast<float*>(cand + (REFINE ? a.candcap : 0));
@@ -255,18 +281,18 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     for (int j = warp; j < count; j += PAIR * NWR) {
       if constexpr (PAIR == 1) {
         const int n = cand_at(j);
-        if (n >= 0) consider(n, warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
+        if (n >= 0) consider(n, warp_dot(rrow, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
         continue;
       }
       const int n1 = cand_at(j), n2 = cand_at(j + NWR);
       if (n1 >= 0 && n2 >= 0) {
-        const float2 c = warp_dot2(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n1 * a.Mp),
+        const float2 c = warp_dot2(rrow, reinterpret_cast<const float4*>(a.At + (int64_t)n1 * a.Mp),
                                    reinterpret_cast<const float4*>(a.At + (int64_t)n2 * a.Mp), q4, lane);
         consider(n1, c.x);
         consider(n2, c.y);
       } else if (n1 >= 0 || n2 >= 0) {
         const int n = n1 >= 0 ? n1 : n2;
-        consider(n, warp_dot(rsm, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
+        consider(n, warp_dot(rrow, reinterpret_cast<const float4*>(a.At + (int64_t)n * a.Mp), q4, lane));
       }
     }
     if (lane == 0) red_c[warp] = best;
@@ -328,19 +354,20 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
+  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM, FSM && (T <= OMP_ZLANE_TMAX)>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
                                                         &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
   if (freq_cta) upd_freq_mark(b == 0 ? 1 : 3);
 #else
-  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM, FSM && (T <= OMP_ZLANE_TMAX)>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
-static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, cudaStream_t st) {
+static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem_rest, size_t persist, cudaStream_t st) {
   auto kern = k_update<SEL, T, CH, MINB, P>;
+  const size_t smem = smem_rest + update_region0<T>(SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM, a.Mp);
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   // (a function attribute is per device: one opt-in per device this process launches on)
   static std::atomic<uint64_t> opted{0};
@@ -460,8 +487,8 @@ cudaError_t launch_update(const UpdateLaunch& L, cudaStream_t st) {
   a.fsm = (refine && fk * 4 <= kFsmMaxBytes && (L.B < 8192 || L.Mp <= OMP_FSM_MP_MAX)) ? 1 : 0;
   // the kept entries of one signal are at most groups x TOPK: a list that size never overflows
   a.candcap = refine ? (int)min((int64_t)RF_CAP, (int64_t)L.groups * TOPK) : 0;
-  const size_t smem = (refine ? (size_t)L.Mp * 4 : (size_t)L.Mp) + (size_t)Sp * 6 * 4 + (size_t)a.candcap * 4 +
-                      (a.fsm ? (size_t)fk * 4 : 0);
+  // (without the first region, whose size depends on the block size: update_region0)
+  const size_t smem = (size_t)Sp * 6 * 4 + (size_t)a.candcap * 4 + (a.fsm ? (size_t)fk * 4 : 0);
   if (refine) return a.fsm ? launch_r<SEL_SCREEN_FSM>(a, L.B, smem, L.l2_persist_bytes, st)
                            : launch_r<SEL_SCREEN>(a, L.B, smem, L.l2_persist_bytes, st);
   if (L.ynorm2) return launch_r<SEL_PROJ>(a, L.B, smem, L.l2_persist_bytes, st);

@@ -263,7 +263,10 @@ struct TailSmem {
 // of A^T in global memory -- the same values, so the same result.
 // FZ8: the row sweep keeps 8 column loads in flight (F_k in L1 / L2); with F_k in shared memory 4 do,
 // and the smaller code keeps more of the kernel in the instruction cache (same FMA order either way).
-template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false, bool FZ8 = true>
+// ZLANE (only with F_k in shared memory, FZ8 = false): z = F^T w thread per column instead of warp per
+// column -- the same bits (see the z loop); pays where it frees warps of a small CTA (T <= 64: c5 at 10^4 /
+// 10^5 signals +4 %, c2 +5.7 %) and costs the 48-register T = 128 variant spills (c3 -2.7 %).
+template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false, bool FZ8 = true, bool ZLANE = false>
 __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
                                                 const float cst, const TailSmem& sm, const float* Fb,
                                                 float* Fs_append, const float4* rows_sm = nullptr,
@@ -299,6 +302,33 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   // takes ZC columns at a time so their loads and shuffle reductions overlap -- ZC changes only the
   // interleaving, not any column's arithmetic)
   constexpr int NW = T / 32;
+  if constexpr (ZLANE && !FZ8) {
+    // F_k in shared memory: thread per column, the same arithmetic without a shuffle.  Thread j forms the
+    // 32 lane partials p_l = sum_{i = l, l+32, ... <= j} F[i, j] w_i (the same FMA chains, from 0) and adds
+    // them in the xor tree's pairing: level o pairs the partials of lanes l and l ^ o (o = 16, 8, 4, 2, 1),
+    // which is the adjacent-pair tree over the leaves in bit-reversed order.  IEEE addition is
+    // commutative, so z_j is bit for bit the warp-per-column result (tests/test_tree_order.py emulates
+    // both).  About a third of the instructions and no shuffle latency chain; reads are conflict-free
+    // (the column offsets j(j+1)/2 of 32 consecutive j fall in 32 distinct banks).
+    for (int j = tid; j < k; j += T) {
+      const float* colj = Fb + (int64_t)j * (j + 1) / 2;
+      float p[32];                      // p[r] = partial of lane brev5(r)
+#pragma unroll
+      for (int r = 0; r < 32; ++r) p[r] = 0.f;
+      for (int i0 = 0; i0 <= j; i0 += 32) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const int i = i0 + (int)(__brev((unsigned)r) >> 27);
+          if (i <= j) p[r] = fmaf(colj[i], w[i], p[r]);
+        }
+      }
+#pragma unroll
+      for (int h = 1; h < 32; h <<= 1)  // adjacent pairs, then pairs of pairs, ...
+#pragma unroll
+        for (int r = 0; r < 32; r += 2 * h) p[r] = p[r] + p[r + h];
+      z[j] = p[0];
+    }
+  } else
   for (int j0 = ZC * warp; j0 < k; j0 += ZC * NW) {
     const float* col[ZC];
     float acc_z[ZC];
@@ -544,7 +574,8 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       }
       // acc[c] = r
       // ||r||^2: one partial per float4 chunk, summed below in an order that does not depend on T
-      if constexpr (!V0) {
+      // (one warp: thread l owns chunks l, l + 32, ... -- it sums them itself, below)
+      if constexpr (!V0 && T != 32) {
         sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));
         if (a.Rb) {   // the bf16 plane's rounding error, for the next window (exact differences)
           const float4 e = make_float4(acc[c].x - __bfloat162float(__float2bfloat16_rn(acc[c].x)),
@@ -580,6 +611,31 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       r2 = block_sum_d<T>(pr);
     }
     rr = (float)r2;
+  } else if constexpr (T == 32) {
+    // the same order from registers: lane l's chunks l, l + 32, ... are its acc[0], acc[1], ...
+    rr = 0.f;
+    float dd = 0.f;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (tid + c * T < q4) {
+        const float4 r = acc[c];
+        rr += fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, r.w * r.w)));
+        if (a.Rb) {
+          const float4 e = make_float4(r.x - __bfloat162float(__float2bfloat16_rn(r.x)),
+                                       r.y - __bfloat162float(__float2bfloat16_rn(r.y)),
+                                       r.z - __bfloat162float(__float2bfloat16_rn(r.z)),
+                                       r.w - __bfloat162float(__float2bfloat16_rn(r.w)));
+          dd += fmaf(e.x, e.x, fmaf(e.y, e.y, fmaf(e.z, e.z, e.w * e.w)));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    if (a.Rb) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    }
+    dn2 = dd;
   } else {
     __syncthreads();
     rr = 0.f;
