@@ -116,14 +116,17 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const bool freq_cta = threadIdx.x == 0 && a.k == g_upd_trace_k && (b == 0 || b == gridDim.x - 1);
   if (freq_cta) upd_freq_mark(b == 0 ? 0 : 2);
 #endif
-  if (a.status[b] != SIG_RUNNING) return;
+  // the status and this signal's row in the current live set, loaded together (one round trip; the
+  // slot of a finished signal is never used)
+  const int status_b = a.status[b];
+  const int cur_slot = a.slot ? a.slot[b] : (int)b;
+  if (status_b != SIG_RUNNING) return;
 #ifdef OMP_UPDATE_TRACE
   unsigned long long upd_t0_ = clock64();
 #endif
   const int k = a.k;
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
-  const int cur_slot = a.slot ? a.slot[b] : (int)b;   // this signal's row in the current live set
   // dynamic shared memory (sizes in launch_update / launch_t):
   //   [update_region0: the fp32 residual row (refine): Mp floats; else Mp / 4 floats; one-warp CTAs: none]
   //   [w, z, u, xs: Sp floats each]
