@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(T, 1) k_small(const SmallArgs s) {
         }
         // one CTA per signal on the critical path: F_k (and, if cached, the support rows) from shared
         // memory; 8 rows in flight, 8 z columns per warp
-        append_residual<T, CH, 8, 8, false, false>(a, b, k, n, sel_c, sm, Fsm, Fsm,
+        append_residual<T, CH, 8, 8, false, 0>(a, b, k, n, sel_c, sm, Fsm, Fsm,
                                                                   s.rows ? rows_sm : nullptr);
       }
       __syncthreads();

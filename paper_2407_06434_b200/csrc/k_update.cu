@@ -356,14 +356,19 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
     return;
   }
   const TailSmem sm{w, z, u, xs, ss, ro, red, reinterpret_cast<float*>(dsm), &sel_n};
+  // the append's load depth: one CTA per SM (MINB = 1: a few signals, F_k of a large S in L2) keeps 4 z
+  // columns x 8 rows and 16 sweep columns in flight; otherwise occupancy hides the latency
+  constexpr int ZCK = (T == 32) ? OMP_ZC32 : (MINB == 1 ? 4 : kZC);
+  constexpr int ZRK = (MINB == 1) ? 8 : 4;
+  constexpr int FZN = FSM ? 0 : (MINB == 1 ? 16 : 8);
 #ifdef OMP_UPDATE_TRACE
-  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM, FSM && (T <= OMP_ZLANE_TMAX)>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
+  append_residual<T, CH, P, ZCK, SEL == SEL_PROJ, FZN, FSM && (T <= OMP_ZLANE_TMAX), ZRK>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
                                                         &upd_t0_);
   UPD_TRACE(11);
   if (threadIdx.x == 0 && a.k == g_upd_trace_k) atomicAdd(&g_upd_clk[15], 1ull);
   if (freq_cta) upd_freq_mark(b == 0 ? 1 : 3);
 #else
-  append_residual<T, CH, P, (T == 32 ? OMP_ZC32 : kZC), SEL == SEL_PROJ, !FSM, FSM && (T <= OMP_ZLANE_TMAX)>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
+  append_residual<T, CH, P, ZCK, SEL == SEL_PROJ, FZN, FSM && (T <= OMP_ZLANE_TMAX), ZRK>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr);
 #endif
 }
 
@@ -415,9 +420,23 @@ static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem_rest, si
 // keeps 8 float4 chunks (8 / CH rows) in flight in the gather instead of 2 rows.  Measured (graph path,
 // profiles/r02/ab/ab_mid_r02m.txt): c2 +2.8 %, M = 1024 at B = 10^3 +2.7 %, t2m1024 at B = 10^3 +6.6 %,
 // but c5 at B = 10^3 (T = 128, CH = 1) -1.2 %, which therefore keeps 2.  OMP_B200_MID=0: off (A/B)
+#ifndef OMP_FEW_TMAX
+#define OMP_FEW_TMAX 512
+#endif
 template <int SEL, int T, int CH>
 static cudaError_t launch_tc(const UpdateArgs& a, int64_t B, size_t smem, size_t persist, bool few, bool mid,
                              cudaStream_t st) {
+  constexpr int Q = T * CH;
+  if (few && (SEL != SEL_SCREEN_FSM || Q >= 512)) {
+    // at most 2 CTAs per SM: wider CTAs (up to 512 threads, one float4 chunk each while the row allows)
+    // so the append's column dots and row sweeps of a large S run on more warps.  Measured
+    // (profiles/r02/ab/ab_few_r02v.txt, ab_few2_r02w.txt): t2m2048 (S = 512) 2.04x, t2m1024 +29 %, c4 at
+    // B = 100 +31 %; with F_k still in shared memory and rows of <= 1024 floats the wide CTA lost (c3 at
+    // B = 200: -8 %), so there it keeps (T, CH).
+    constexpr int TF = Q < OMP_FEW_TMAX ? Q : OMP_FEW_TMAX;
+    constexpr int CHF = Q / TF;
+    return launch_t<SEL, TF, CHF, 1, (16 / CHF > 2 ? 16 / CHF : 2)>(a, B, smem, persist, st);
+  }
   if (few) return launch_t<SEL, T, CH, 1, (16 / CH > 2 ? 16 / CH : 2)>(a, B, smem, persist, st);
   if constexpr ((T <= 64 && CH <= 2) || (T == 128 && CH == 2))
     if (mid) return launch_t<SEL, T, CH, 8, (8 / CH > 2 ? 8 / CH : 2)>(a, B, smem, persist, st);

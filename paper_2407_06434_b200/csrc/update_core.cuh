@@ -261,12 +261,15 @@ struct TailSmem {
 // rows_sm (nullable): a shared-memory copy of the support's atom rows (row j at rows_sm + j q4,
 // j <= k; row k may still be landing by cp.async, waited for here) that the gather reads instead
 // of A^T in global memory -- the same values, so the same result.
-// FZ8: the row sweep keeps 8 column loads in flight (F_k in L1 / L2); with F_k in shared memory 4 do,
+// FZN: the row sweep keeps FZN (8, or 16 in the one-CTA-per-SM variant) column loads in flight (F_k in
+// L1 / L2); FZN = 0: F_k in shared memory, where 4 do,
 // and the smaller code keeps more of the kernel in the instruction cache (same FMA order either way).
-// ZLANE (only with F_k in shared memory, FZ8 = false): z = F^T w thread per column instead of warp per
+// ZLANE (only with F_k in shared memory, FZN = 0): z = F^T w thread per column instead of warp per
 // column -- the same bits (see the z loop); pays where it frees warps of a small CTA (T <= 64: c5 at 10^4 /
 // 10^5 signals +4 %, c2 +5.7 %) and costs the 48-register T = 128 variant spills (c3 -2.7 %).
-template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false, bool FZ8 = true, bool ZLANE = false>
+// ZR: rows of a column whose loads the warp-per-column z keeps in flight (4; 8 in the one-CTA-per-SM
+// variant, where F_k of a large S is read from L2 one column group at a time).
+template <int T, int CH, int P = 2, int ZC = 2, bool V0 = false, int FZN = 8, bool ZLANE = false, int ZR = 4>
 __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64_t b, const int k, const int n,
                                                 const float cst, const TailSmem& sm, const float* Fb,
                                                 float* Fs_append, const float4* rows_sm = nullptr,
@@ -302,7 +305,7 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   // takes ZC columns at a time so their loads and shuffle reductions overlap -- ZC changes only the
   // interleaving, not any column's arithmetic)
   constexpr int NW = T / 32;
-  if constexpr (ZLANE && !FZ8) {
+  if constexpr (ZLANE && FZN == 0) {
     // F_k in shared memory: thread per column, the same arithmetic without a shuffle.  Thread j forms the
     // 32 lane partials p_l = sum_{i = l, l+32, ... <= j} F[i, j] w_i (the same FMA chains, from 0) and adds
     // them in the xor tree's pairing: level o pairs the partials of lanes l and l ^ o (o = 16, 8, 4, 2, 1),
@@ -339,18 +342,18 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     }
     const int jl = min(j0 + ZC, k) - 1;   // last column of the group
     int i = lane;
-    // long columns (F_k of a large S lives in L2): four rows' loads in flight, FMAs in the same order
-    for (; i + 96 <= jl; i += 128) {
-      float cv[4][ZC], wv[4];
+    // long columns (F_k of a large S lives in L2): ZR rows' loads in flight, FMAs in the same order
+    for (; i + 32 * (ZR - 1) <= jl; i += 32 * ZR) {
+      float cv[ZR][ZC], wv[ZR];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < ZR; ++q) {
         const int ii = i + 32 * q;
         wv[q] = w[ii];
 #pragma unroll
         for (int c = 0; c < ZC; ++c) cv[q][c] = (ii <= j0 + c && j0 + c < k) ? col[c][ii] : 0.f;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < ZR; ++q)
 #pragma unroll
         for (int c = 0; c < ZC; ++c)
           if (i + 32 * q <= j0 + c && j0 + c < k) acc_z[c] = fmaf(cv[q][c], wv[q], acc_z[c]);
@@ -400,16 +403,17 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
     int j = i & ~31;
     int o = j * (j + 1) / 2 + i;                  // offset of F[i, j] in the packed columns
-    // 8 column loads in flight (F_k of a large S lives in L2, not L1), the FMAs in the same order
-    if constexpr (FZ8) for (; j + 8 <= k; j += 8) {
-      float f[8];
+    // FZN column loads in flight (F_k of a large S lives in L2, not L1), the FMAs in the same order
+    // (column j always goes to partial j mod 4, whatever the blocking)
+    if constexpr (FZN > 0) for (; j + FZN <= k; j += FZN) {
+      float f[FZN > 0 ? FZN : 1];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < FZN; ++q) {
         f[q] = (j + q >= i) ? Fb[o] : 0.f;
         o += j + q + 1;
       }
 #pragma unroll
-      for (int g = 0; g < 8; g += 4) {
+      for (int g = 0; g < FZN; g += 4) {
         v0 = fmaf(f[g], z[j + g], v0);
         t0 = fmaf(f[g], u[j + g], t0);
         v1 = fmaf(f[g + 1], z[j + g + 1], v1);
