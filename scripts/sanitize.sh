@@ -10,7 +10,7 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ $tool = memcheck ] && extra="--leak-check full"
-  for paths in "bf16 3xtf32 simt small proj host densify correlate" "proj_simt"; do
+  for paths in "bf16 3xtf32 simt small proj host densify correlate" "proj_simt" "variants"; do
     echo "=== $tool: $paths" >> $OUT/sanitize_${TAG}_${tool}.txt
     if [ "$paths" = proj_simt ]; then envp="OMP_B200_P0=simt"; else envp=""; fi
     env $envp timeout 1500 $CS --tool $tool $extra --error-exitcode 17 --target-processes all \

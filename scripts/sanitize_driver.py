@@ -4,7 +4,8 @@
 
 Paths: bf16, 3xtf32, simt (screened residual path in each correlation mode, direct launches and the
 CUDA-graph replay), small (the persistent small-batch kernel), proj (the projection path, 3xTF32 P0),
-proj_simt (the projection path with the SIMT P0 GEMM), host (ompBatchHost, chunked), densify, correlate.
+proj_simt (the projection path with the SIMT P0 GEMM), host (ompBatchHost, chunked), densify, correlate,
+variants (the update's one-warp and 512-thread launch shapes).
 Shapes: tiny and c2-like with a ragged B, eps stops on half the signals.  Each result is checked
 for sanity (statuses, supports in range) so a silent corruption also fails the run.
 """
@@ -78,6 +79,14 @@ def run(path, M, N, B, S, seed):
 def main(paths):
     paths = paths or ["bf16", "3xtf32", "simt", "small", "proj", "host", "densify", "correlate"]
     for path in paths:
+        if path == "variants":
+            # the update's launch-shape variants the shapes above do not reach: one warp per signal
+            # (B >= 8192 at M <= 512: no staged residual row, ||r||^2 in registers), and one CTA of 512
+            # threads per SM (B <= 2 x SMs at M = 2048, F_k in L2 from k = 64)
+            for (M, N, B, S) in ((512, 1024, 8200, 3), (2048, 4096, 12, 68)):
+                run("bf16", M, N, B, S, 7)
+            print("sanitize_driver: variants ok", flush=True)
+            continue
         for (M, N, B, S) in ((32, 64, 16, 4), (256, 1024, 300 if path != "small" else 12, 32)):
             run(path, M, N, B, S, 7)
         print(f"sanitize_driver: {path} ok", flush=True)
