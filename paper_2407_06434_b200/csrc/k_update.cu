@@ -466,7 +466,12 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
     const char* e = getenv("OMP_B200_MID");
     mid_env = (e && e[0] == '0') ? 0 : 1;
   }
-  const bool mid = mid_env && B <= 8 * (int64_t)sms;
+  static int64_t mid_maxb = -1;       // OMP_B200_MID_MAXB: the largest batch that takes "mid" (A/B)
+  if (mid_maxb < 0) {
+    const char* e = getenv("OMP_B200_MID_MAXB");
+    mid_maxb = e ? atoll(e) : 8 * (int64_t)sms;
+  }
+  const bool mid = mid_env && B <= mid_maxb;
   const int64_t q4 = a.Mp / 4;
   // Large batches of narrow rows (many waves: throughput) take one warp per signal and 32 signals per
   // SM; smaller batches keep the wider CTAs, whose shorter per-signal chain sets the launch time when
