@@ -236,6 +236,14 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
   // programmatic dependent launch: the next kernel (the update) may start launching now; it waits
   // for this grid's completion itself (griddepcontrol.wait) before touching anything this writes
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // the TMA descriptors (kernel parameters) are fetched now, under the prologue, not at the first load
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int p = 0; p < K_::NPLANES; ++p) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.r[p])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a[p])) : "memory");
+    }
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) {
@@ -361,9 +369,14 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
       sched.coords(t - z * tiles_mn, tm, tn);
       const int a = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
+      const int row = tm * BM * CG + (int)rank * BM + lg * 32 + lane;
+      // this row's window, loaded before waiting for the accumulator (its round trip overlaps the MMAs)
+      float rs = 0.f;
+      if constexpr (MODE == MODE_TOPK) {
+        if (row < rows) rs = __ldg(ep.rslot + row);
+      }
       mbar_wait(&tfull[a], aphase);
       fence_after();
-      const int row = tm * BM * CG + (int)rank * BM + lg * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * BN + half * HB);
       const int64_t colh = (int64_t)tn * BN + half * HB;
       bool live = row < rows;
@@ -394,7 +407,7 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
         // reaching max - W and emit their in-window entries in index order (predicated stores; at
         // most TOPK, an overflow is flagged in the last slot with the half-tile maximum).
         float W = 0.f;
-        if (live) W = ep.window * ep.rslot[row];
+        if (live) W = ep.window * rs;
         float cm[HB / 32];
         float tmax = 0.f;
 #pragma unroll
