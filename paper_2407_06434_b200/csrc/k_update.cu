@@ -99,9 +99,10 @@ constexpr int SEL_SCREEN_FSM = 3;   // SEL_SCREEN with the packed F_k staged in 
 #ifndef OMP_RG
 #define OMP_RG 1
 #endif
-template <int T>
+template <int T, int CH>
 __host__ __device__ constexpr size_t update_region0(bool refine, int64_t Mp) {
-  return (T == 32 && OMP_RG) ? 0 : (refine ? (size_t)Mp * 4 : (size_t)Mp);
+  // (one-warp CTAs that do not own their summation-order chunks keep the chunk partials: 2 Mp / 4 floats)
+  return (T == 32 && OMP_RG) ? (update_rreg<T, CH>() ? 0 : (size_t)Mp * 2) : (refine ? (size_t)Mp * 4 : (size_t)Mp);
 }
 
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   const int q4 = (int)(a.Mp >> 2);
   const int Sp = (k + 4) & ~3;          // >= k + 1, multiple of 4
   // dynamic shared memory (sizes in launch_update / launch_t):
-  //   [update_region0: the fp32 residual row (refine): Mp floats; else Mp / 4 floats; one-warp CTAs: none]
+  //   [update_region0: the fp32 residual row (refine): Mp floats; else Mp / 4 floats; one-warp CTAs: none,
+  //    or the 2 Mp / 4 chunk partials of ||r||^2 where they cannot be summed in registers]
   //   [w, z, u, xs: Sp floats each]
   //   [ss, ro: Sp ints each] [cand: a.candcap ints (refine)] [F_k packed (fsm)]
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   constexpr bool RG = (T == 32) && OMP_RG;
   float4* rsm = reinterpret_cast<float4*>(dsm);
   // (the first region doubles as the tail's ||r||^2 chunk partials, Mp / 4 floats, after the refine)
-  float* w = reinterpret_cast<float*>(dsm + update_region0<T>(REFINE, a.Mp));
+  float* w = reinterpret_cast<float*>(dsm + update_region0<T, CH>(REFINE, a.Mp));
   float* z = w + Sp;
   float* u = z + Sp;
   float* xs = u + Sp;
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
 template <int SEL, int T, int CH, int MINB = (OMP_UPDATE_CTAS / T < 32 ? OMP_UPDATE_CTAS / T : 32), int P = 2>
 static cudaError_t launch_t(const UpdateArgs& a, int64_t B, size_t smem_rest, size_t persist, cudaStream_t st) {
   auto kern = k_update<SEL, T, CH, MINB, P>;
-  const size_t smem = smem_rest + update_region0<T>(SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM, a.Mp);
+  const size_t smem = smem_rest + update_region0<T, CH>(SEL == SEL_SCREEN || SEL == SEL_SCREEN_FSM, a.Mp);
   // static + dynamic shared memory may exceed the 48 KB default: opt in once per variant
   // (a function attribute is per device: one opt-in per device this process launches on)
   static std::atomic<uint64_t> opted{0};

@@ -31,6 +31,19 @@
 
 namespace ompb {
 
+// OMP_V8 = 1: 256-bit atom-row loads in the gather and the chunk-pair ownership that goes with them.
+// Off: the probe's 256-bit gather is 2.5 % (c4) / 6 % (c5) faster than its 128-bit one, but in the
+// update it lost (c4 -5 %, c5 B = 10^5 -4 %, c3 -5 %, c2 +0.8 %; profiles/r02/ab/ab_v8_r02ad.txt)
+#ifndef OMP_V8
+#define OMP_V8 0
+#endif
+// does a CTA of T threads own, per thread, exactly the chunks lane l of warp 0 sums for ||r||^2, in
+// that order (so it may sum them in registers)?  Only one-warp CTAs, with the matching ownership.
+template <int T, int CH>
+__host__ __device__ constexpr bool update_rreg() {
+  return T == 32 && (OMP_V8 == 0 || CH % 2 == 0);
+}
+
 struct UpdateArgs {
   int32_t k, S;
   int32_t fsm;          // k_update: the packed F_k is staged in shared memory
@@ -116,6 +129,12 @@ __device__ __forceinline__ float4 ldg_policy(const float4* ptr, uint64_t pol) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
   return v;
+}
+// 256-bit load (LDG.E.256 on sm_100a): two adjacent float4 chunks
+__device__ __forceinline__ void ldg8_policy(const float* ptr, uint64_t pol, float4& lo, float4& hi) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+               : "l"(ptr), "l"(pol));
 }
 __device__ __forceinline__ void stg_policy(float4* ptr, float4 v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
@@ -484,10 +503,19 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   // A compile-time choice: both kernels' (T, CH) maps give T x CH = the power of two >= Mp / 4 (>= 32),
   // so T x CH <= 256 <=> Mp <= 1024 in k_update and k_small alike.
   constexpr bool yfirst = T * CH <= 256;
+  // Chunk ownership: with OMP_V8 and an even CH (V8) thread t owns the float4 chunk PAIRS t, t + T, ...
+  // (one 256-bit load per pair and row), else the chunks t, t + T, ...; qidx(c) = the float4 chunk of slot c.
+  // Nothing elementwise depends on it.  ||r||^2 sums its per-chunk partials in ONE order for every
+  // kernel and block size: lane l of warp 0 takes chunks l, l + 32, ... ascending (OMP_V8: chunks
+  // 2(l + 32 i) + e, i ascending, e = 0, 1), then the xor tree.  A one-warp CTA owns exactly
+  // lane l's chunks in that order when V8 (or OMP_V8 = 0) holds, and sums them in registers (RREG).
+  constexpr bool V8 = (OMP_V8 != 0) && (CH % 2 == 0);
+  constexpr bool RREG = update_rreg<T, CH>();
+  auto qidx = [&](int c) -> int { return V8 ? 2 * (tid + (c >> 1) * T) + (c & 1) : tid + c * T; };
   const float* y = a.Y + b * a.ldy;
   const bool yvec = ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) && (a.ldy % 4 == 0);
   auto load_y = [&](int c) {
-    const int q = tid + c * T;
+    const int q = qidx(c);
     const int64_t m = (int64_t)q << 2;
     float4 v;
     if (yvec && m + 3 < a.M) {
@@ -504,7 +532,7 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const int q = tid + c * T;
+      const int q = qidx(c);
       if (q >= q4 || !yfirst) {
         acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
@@ -517,7 +545,7 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     // chunk c of this thread exists for every row (T * CH == q4 at the benchmark shapes: no predicate)
     bool has[CH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) has[c] = (T * CH == q4) || (tid + c * T < q4);
+    for (int c = 0; c < CH; ++c) has[c] = (T * CH == q4) || (qidx(c) < q4);
     // fold (-)x_j times row j into acc, j ascending; rows come P at a time (loads before FMAs)
     const bool full = (T * CH == q4);
     auto fold = [&](const float x, const float4 (&v)[CH]) {
@@ -548,29 +576,37 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     };
     if (rows_sm) {
       gather([&](int j, float4 (&v)[CH]) {
-        const float4* r = rows_sm + (size_t)j * q4 + tid;
+        const float4* r = rows_sm + (size_t)j * q4;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) v[c] = has[c] ? r[c * T] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < CH; ++c) v[c] = has[c] ? r[qidx(c)] : make_float4(0.f, 0.f, 0.f, 0.f);
       });
     } else if (full) {           // every chunk exists: unpredicated loads (measured: the predicated form
                                  // alone doubled the c4 update's time)
-      gather([&](int j, float4 (&v)[CH]) {
-        const float4* r = A4 + ro[j];
+      if constexpr (V8) {
+        gather([&](int j, float4 (&v)[CH]) {
+          const float* r = a.At + ((size_t)ro[j] << 2) + (size_t)tid * 8;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) v[c] = ldg_policy(r + c * T, keep);
-      });
+          for (int c = 0; c < CH; c += 2) ldg8_policy(r + (size_t)(c >> 1) * T * 8, keep, v[c], v[c + 1]);
+        });
+      } else {
+        gather([&](int j, float4 (&v)[CH]) {
+          const float4* r = A4 + ro[j];
+#pragma unroll
+          for (int c = 0; c < CH; ++c) v[c] = ldg_policy(r + c * T, keep);
+        });
+      }
     } else {
       gather([&](int j, float4 (&v)[CH]) {
-        const float4* r = A4 + ro[j];
+        const float4* r = reinterpret_cast<const float4*>(a.At) + ro[j];
 #pragma unroll
-        for (int c = 0; c < CH; ++c) v[c] = has[c] ? ldg_policy(r + c * T, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < CH; ++c) v[c] = has[c] ? ldg_policy(r + qidx(c), keep) : make_float4(0.f, 0.f, 0.f, 0.f);
       });
     }
   }
   OMP_TAIL_TRACE(4);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    const int q = tid + c * T;
+    const int q = qidx(c);
     if (q < q4) {
       if (!yfirst) {
         const float4 yv = load_y(c);
@@ -578,8 +614,8 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       }
       // acc[c] = r
       // ||r||^2: one partial per float4 chunk, summed below in an order that does not depend on T
-      // (one warp: thread l owns chunks l, l + 32, ... -- it sums them itself, below)
-      if constexpr (!V0 && T != 32) {
+      // (RREG: the one warp owns its chunks in the summation order -- it sums them itself, below)
+      if constexpr (!V0 && !RREG) {
         sm.pr[q] = fmaf(acc[c].x, acc[c].x, fmaf(acc[c].y, acc[c].y, fmaf(acc[c].z, acc[c].z, acc[c].w * acc[c].w)));
         if (a.Rb) {   // the bf16 plane's rounding error, for the next window (exact differences)
           const float4 e = make_float4(acc[c].x - __bfloat162float(__float2bfloat16_rn(acc[c].x)),
@@ -615,13 +651,13 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
       r2 = block_sum_d<T>(pr);
     }
     rr = (float)r2;
-  } else if constexpr (T == 32) {
-    // the same order from registers: lane l's chunks l, l + 32, ... are its acc[0], acc[1], ...
+  } else if constexpr (RREG) {
+    // the same order from registers: lane l's chunks, in the summation order, are its acc[0], acc[1], ...
     rr = 0.f;
     float dd = 0.f;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      if (tid + c * T < q4) {
+      if (qidx(c) < q4) {
         const float4 r = acc[c];
         rr += fmaf(r.x, r.x, fmaf(r.y, r.y, fmaf(r.z, r.z, r.w * r.w)));
         if (a.Rb) {
@@ -644,12 +680,26 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
     __syncthreads();
     rr = 0.f;
     float dd = 0.f;
-    if (warp == 0) {                    // lane l: chunks l, l + 32, ... ascending, then the xor tree
-      for (int q = lane; q < q4; q += 32) rr += sm.pr[q];
+    if (warp == 0) {                    // lane l: its chunks in the summation order, then the xor tree
+      if constexpr (OMP_V8 != 0) {
+        for (int q = 2 * lane; q < q4; q += 64) {
+          rr += sm.pr[q];
+          if (q + 1 < q4) rr += sm.pr[q + 1];
+        }
+      } else {
+        for (int q = lane; q < q4; q += 32) rr += sm.pr[q];
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
       if (a.Rb) {
-        for (int q = lane; q < q4; q += 32) dd += sm.pr[q4 + q];
+        if constexpr (OMP_V8 != 0) {
+          for (int q = 2 * lane; q < q4; q += 64) {
+            dd += sm.pr[q4 + q];
+            if (q + 1 < q4) dd += sm.pr[q4 + q + 1];
+          }
+        } else {
+          for (int q = lane; q < q4; q += 32) dd += sm.pr[q4 + q];
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
       }
@@ -682,7 +732,7 @@ __device__ __forceinline__ void append_residual(const UpdateArgs& a, const int64
   const int64_t ro_out = (int64_t)ns * a.Mp;
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    const int q = tid + c * T;
+    const int q = qidx(c);
     if (q < q4) {
       const float4 r = acc[c];
       if (a.R32) stg_policy(reinterpret_cast<float4*>(a.R32 + ro_out) + q, r, stream);

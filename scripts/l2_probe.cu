@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -133,6 +134,56 @@ __global__ void __launch_bounds__(T, 1024 / T) k_gather(const float4* __restrict
   }
 }
 
+// the same gather with 256-bit loads (ld.global.v8.f32, LDG.E.256 on sm_100a): CH8 float8 chunks per
+// thread and row (T * CH8 * 8 == row length)
+__device__ __forceinline__ void ldg8_keep(const float* ptr, uint64_t pol, float (&v)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(ptr), "l"(pol));
+}
+template <int T, int CH8, int P>
+__global__ void __launch_bounds__(T, 1024 / T) k_gather8(const float* __restrict__ table, const uint32_t* __restrict__ idx,
+                                                         int rows, float* out, Clk* clk) {
+  const uint64_t pol = policy_evict_last();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    clk->c0 = clock64();
+    clk->t0 = gtimer();
+  }
+  const int row_len = T * CH8 * 8;
+  const uint32_t* id = idx + (int64_t)blockIdx.x * rows;
+  float acc[CH8][8];
+#pragma unroll
+  for (int c = 0; c < CH8; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[c][e] = 0.f;
+  int j = 0;
+  for (; j + P <= rows; j += P) {
+    float v[P][CH8][8];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float* r = table + (int64_t)id[j + p] * row_len + threadIdx.x * 8;
+#pragma unroll
+      for (int c = 0; c < CH8; ++c) ldg8_keep(r + c * T * 8, pol, v[p][c]);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int c = 0; c < CH8; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[c][e] = fmaf(0.5f, v[p][c][e], acc[c][e]);
+  }
+  float r = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH8; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) r += acc[c][e];
+  if (r == 1234.5f) out[blockIdx.x] = r;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    clk->c1 = clock64();
+    clk->t1 = gtimer();
+  }
+}
+
 template <typename F>
 static void timed(const char* name, double bytes, int reps, F launch, Clk* dclk) {
   cudaEvent_t a, b;
@@ -181,7 +232,9 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&buf, big));
   CK(cudaMemset(buf, 0, big));
 
+  const bool only_v8 = argc > 2 && std::string(argv[2]) == "v8";   // just the 128- vs 256-bit gather
   for (int64_t mb : {4, 32, 64, 96}) {
+    if (only_v8) break;
     const int64_t bytes = mb << 20;
     char name[64];
     snprintf(name, sizeof name, "stream_l2_%lldMB", (long long)mb);
@@ -190,7 +243,8 @@ int main(int argc, char** argv) {
       k_stream<<<sms * 8, 256>>>(buf, bytes / 16, passes, out, clk);
     }, clk);
   }
-  timed("stream_hbm_1GB", (double)big, reps, [&] { k_stream<<<sms * 8, 256>>>(buf, big / 16, 1, out, clk); }, clk);
+  if (!only_v8)
+    timed("stream_hbm_1GB", (double)big, reps, [&] { k_stream<<<sms * 8, 256>>>(buf, big / 16, 1, out, clk); }, clk);
 
   // gather: c4 shape (rows of 2048 floats from 8192), 65 rows per CTA, 12500 CTAs ~ one c4 launch at k = 64
   const int nsig = 12500, rows = 65;
@@ -205,6 +259,20 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
   const double gb = (double)nsig * rows * 2048 * 4;
   timed("gather_c4_T128_CH4_P2", gb, reps, [&] { k_gather<128, 4, 2><<<nsig, 128>>>(buf, idx, rows, out, clk); }, clk);
+  const float* fbuf = reinterpret_cast<const float*>(buf);
+  timed("gather8_c4_T128_CH2_P2", gb, reps, [&] { k_gather8<128, 2, 2><<<nsig, 128>>>(fbuf, idx, rows, out, clk); }, clk);
+  timed("gather8_c4_T128_CH2_P4", gb, reps, [&] { k_gather8<128, 2, 4><<<nsig, 128>>>(fbuf, idx, rows, out, clk); }, clk);
+  timed("gather8_c4_T256_CH1_P4", gb, reps, [&] { k_gather8<256, 1, 4><<<nsig, 256>>>(fbuf, idx, rows, out, clk); }, clk);
+  if (only_v8) {
+    for (auto& v : h) v %= 2048;
+    CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    const double g5v = (double)nsig * rows * 512 * 4;
+    timed("gather_c5_T128_CH1_P2", g5v, reps, [&] { k_gather<128, 1, 2><<<nsig, 128>>>(buf, idx, rows, out, clk); }, clk);
+    timed("gather_c5_T32_CH4_P2", g5v, reps, [&] { k_gather<32, 4, 2><<<nsig, 32>>>(buf, idx, rows, out, clk); }, clk);
+    timed("gather8_c5_T32_CH2_P2", g5v, reps, [&] { k_gather8<32, 2, 2><<<nsig, 32>>>(fbuf, idx, rows, out, clk); }, clk);
+    timed("gather8_c5_T64_CH1_P4", g5v, reps, [&] { k_gather8<64, 1, 4><<<nsig, 64>>>(fbuf, idx, rows, out, clk); }, clk);
+    return 0;
+  }
   timed("gather_c4_T128_CH4_P4", gb, reps, [&] { k_gather<128, 4, 4><<<nsig, 128>>>(buf, idx, rows, out, clk); }, clk);
   timed("gather_c4_T256_CH2_P4", gb, reps, [&] { k_gather<256, 2, 4><<<nsig, 256>>>(buf, idx, rows, out, clk); }, clk);
   timed("gather_c4_T512_CH1_P8", gb, reps, [&] { k_gather<512, 1, 8><<<nsig, 512>>>(buf, idx, rows, out, clk); }, clk);
