@@ -30,8 +30,20 @@ namespace tc {
 constexpr int BM = 128;       // signal rows per CTA (UMMA M per CTA)
 constexpr int BN = 256;       // atoms per tile (UMMA N)
 constexpr int GM = 16;        // row-blocks per raster group
-constexpr int EPI_THREADS = 256;   // warps 4..11: two warps per TMEM lane group, 128 columns each
-constexpr int NUM_THREADS = 128 + EPI_THREADS;
+// Epilogue warps EW: 8 (two per TMEM lane group, 128 columns each) or 16 (four per lane group, 64
+// columns each, the two warps of a 128-atom partial group merging their in-window lists through shared
+// memory).  At small K a tile's MMAs are short and 8 warps' epilogue is not hidden behind the next
+// tile's (c5, K = 512: tensor pipe 50 % busy); at K = 2048 the 16 warps cost the MMA-bound screen 2 %.
+// The launch picks 16 below K = OMP_EPI16_KMAX (measured, profiles/r02/ab/ab_epi16_r02ag.txt).
+#ifndef OMP_EPI16_KMAX
+#define OMP_EPI16_KMAX 1536
+#endif
+__host__ __device__ constexpr int epi_threads(int ew) { return 32 * ew; }
+__host__ __device__ constexpr int num_threads(int ew) { return 128 + 32 * ew; }
+// shared memory of the 16-warp epilogue: pair exchange (max, count) and each thread's kept entries
+__host__ __device__ constexpr uint32_t epi_smem(int ew) {
+  return ew == 16 ? (2u * 4u * 2u * 32u * 8u + 16u * 32u * TOPK * 8u) : 0u;
+}
 constexpr int MODE_STORE = 0, MODE_TOPK = 1;
 
 // Operand kinds.  Every stage holds one 128-byte-wide K slab of each plane.
@@ -56,7 +68,7 @@ struct Cfg {
   static constexpr uint32_t A_BYTES = BN_CTA * K_::BK * K_::ELEM;    // one plane of the A tile
   static constexpr uint32_t STAGE_BYTES = K_::NPLANES * (R_BYTES + A_BYTES);
   static constexpr int STAGES = (int)((200u * 1024u) / STAGE_BYTES) < 8 ? (int)((200u * 1024u) / STAGE_BYTES) : 8;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;   // + epi_smem(EW)
   static constexpr uint32_t IDESC = (1u << 4)                            // D = F32
                                     | (K_::FMT << 7) | (K_::FMT << 10)   // A, B formats
                                     | ((uint32_t)(BN >> 3) << 17)        // N
@@ -228,8 +240,8 @@ struct Maps {
   CUtensorMap a[2];         // A^T planes
 };
 
-template <int KIND, int CG, int MODE>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int KIND, int CG, int MODE, int EW>
+__global__ void __launch_bounds__(num_threads(EW), 1)
 k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m, int tiles_n, EpiArgs ep) {
   using C_ = Cfg<KIND, CG>;
   using K_ = Kind<KIND>;
@@ -265,7 +277,7 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_THREADS * CG);
+      mbar_init(&tempty[a], epi_threads(EW) * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -371,10 +383,18 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
     }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global =====================
-    // Eight warps: warp w reads TMEM lane group (w % 4) (hardware rule: warp i owns lanes
-    // 32 (i % 4) .. +31) and the column half (w - 4) / 4, i.e. 128 atoms of the 256-atom tile.
-    const int ew = warp - 4, lg = ew & 3, half = ew >> 2;
-    constexpr int HB = BN / 2;
+    // Warp w reads TMEM lane group (w % 4) (hardware rule: warp i owns lanes 32 (i % 4) .. +31) and the
+    // column part (w - 4) / 4 of the 256-atom tile: CB = 128 (8 warps) or 64 (16 warps) atoms.
+    const int ew = warp - 4, lg = ew & 3, part = ew >> 2;
+    constexpr int HB = BN / (EW / 4);                      // accumulator columns per epilogue warp
+    constexpr int CB = HB;
+    const int half = part * CB / SCREEN_GROUP;            // the 128-atom partial group of this part
+    const int sub = (part * CB / (SCREEN_GROUP / 2)) & 1;  // 16 warps: its lower / upper 64 atoms
+    // 16 warps: [group half][lane group][sub][lane] maxima and counts, [epilogue warp][lane][TOPK] entries
+    float* xm = reinterpret_cast<float*>(tmem_slot + 4);
+    int* xc = reinterpret_cast<int*>(xm + 2 * 4 * 2 * 32);
+    float2* ent = reinterpret_cast<float2*>(xc + 2 * 4 * 2 * 32) + ((size_t)ew * 32 + lane) * TOPK;
+    const int xi = ((half * 4 + lg) * 2) * 32 + lane;      // + sub * 32: this warp's slot
     int it = 0;
     for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
       const int z = t / tiles_mn;
@@ -390,8 +410,8 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
       }
       mbar_wait(&tfull[a], aphase);
       fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * BN + half * HB);
-      const int64_t colh = (int64_t)tn * BN + half * HB;
+      const uint32_t taddr = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * BN + part * HB);
+      const int64_t colh = (int64_t)tn * BN + part * HB;
       bool live = row < rows;
       if constexpr (MODE == MODE_STORE) {
 #pragma unroll 1
@@ -436,8 +456,53 @@ k1_corr_tc(const __grid_constant__ Maps maps, int rows, int num_kb, int tiles_m,
             tmax = fmaxf(tmax, m);
           }
         }
-        const float thr = tmax - W;
         float2* dst = ep.part + ((int64_t)row * (2 * tiles_n) + 2 * tn + half) * TOPK;
+        if constexpr (EW == 16) {
+          // The two warps of this 128-atom group (sub = 0: atoms 0..63, 1: 64..127) exchange their maxima
+          // (named barrier 1 + half * 4 + lg, 64 threads), take the in-window entries of their own 64
+          // atoms, exchange the counts, and store the group's list in index order: the lower warp's
+          // entries first, then the upper's, -1 padding, and with more than TOPK the overflow flag
+          // (group maximum) in the last slot -- exactly the 8-warp epilogue's list for the group.
+          const int bar_id = 1 + half * 4 + lg;
+          xm[xi + sub * 32] = tmax;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          tmax = fmaxf(tmax, xm[xi + (sub ^ 1) * 32]);
+          const float thr = tmax - W;
+          int cnt = 0;
+#pragma unroll
+          for (int c = 0; c < HB / 32; ++c) {
+            const bool need = live && cm[c] >= thr;
+            if (!__any_sync(0xffffffffu, need)) continue;       // warp-uniform: tcgen05.ld is .aligned
+            float v[32];
+            tmem_ld32(taddr + (uint32_t)(c * 32), v);
+            if (need) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) {
+                const float s = fabsf(v[q]);
+                if (s >= thr) {
+                  if (cnt < TOPK) ent[cnt] = make_float2(s, __int_as_float((int)colh + c * 32 + q));
+                  ++cnt;
+                }
+              }
+            }
+          }
+          xc[xi + sub * 32] = cnt;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          const int other = xc[xi + (sub ^ 1) * 32];
+          const int total = cnt + other, base = sub ? other : 0;
+          if (live) {
+            for (int i = 0; i < cnt && base + i < TOPK; ++i)
+              if (!(total > TOPK && base + i == TOPK - 1)) dst[base + i] = ent[i];
+            if (sub) {
+              for (int j = total; j < TOPK; ++j) dst[j] = make_float2(-1.f, __int_as_float(-1));
+              if (total > TOPK) dst[TOPK - 1] = make_float2(tmax, __int_as_float(SEL_OVERFLOW));
+            }
+          }
+          fence_before();
+          mbar_arrive_cta0(&tempty[a]);
+          continue;
+        }
+        const float thr = tmax - W;
         int cnt = 0;
 #pragma unroll
         for (int c = 0; c < HB / 32; ++c) {
@@ -520,8 +585,8 @@ static int num_sms() {
   return n > 0 ? n : 148;
 }
 
-template <int KIND, int CG, int MODE>
-static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const EpiArgs& ep, cudaStream_t st) {
+template <int KIND, int CG, int MODE, int EW>
+static cudaError_t launch_ew(const Operand& R, const Operand& At, int64_t K, const EpiArgs& ep, cudaStream_t st) {
   using C_ = Cfg<KIND, CG>;
   using K_ = Kind<KIND>;
   if (R.rows == 0) return cudaSuccess;
@@ -536,8 +601,9 @@ static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const 
     maps.r[1] = maps.r[0];
     maps.a[1] = maps.a[0];
   }
-  auto kern = k1_corr_tc<KIND, CG, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+  auto kern = k1_corr_tc<KIND, CG, MODE, EW>;
+  const uint32_t smem = C_::SMEM + epi_smem(EW);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int tiles_m = (int)((R.rows + BM * CG - 1) / (BM * CG));
   const int tiles_n = (int)(At.rows / BN);
@@ -548,8 +614,8 @@ static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const 
   const int clusters = tiles < max_clusters ? tiles : max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(clusters * CG));
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = C_::SMEM;
+  cfg.blockDim = dim3(num_threads(EW));
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -561,6 +627,16 @@ static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const 
   cfg.attrs = attr;
   cfg.numAttrs = (MODE == MODE_TOPK && pdl_enabled(1)) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, maps, (int)R.rows, (int)(K / K_::BK), tiles_m, tiles_n, ep);
+}
+
+template <int KIND, int CG, int MODE>
+static cudaError_t launch(const Operand& R, const Operand& At, int64_t K, const EpiArgs& ep, cudaStream_t st) {
+  static int64_t kmax = -1;   // OMP_B200_EPI16_KMAX overrides the crossover (A/B)
+  if (kmax < 0) {
+    const char* e = getenv("OMP_B200_EPI16_KMAX");
+    kmax = e ? atoll(e) : OMP_EPI16_KMAX;
+  }
+  return K < kmax ? launch_ew<KIND, CG, MODE, 16>(R, At, K, ep, st) : launch_ew<KIND, CG, MODE, 8>(R, At, K, ep, st);
 }
 
 template <int MODE>
