@@ -361,8 +361,14 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   // the append's load depth: one CTA per SM (MINB = 1: a few signals, F_k of a large S in L2) keeps 4 z
   // columns x 8 rows and 16 sweep columns in flight; otherwise occupancy hides the latency
   constexpr int ZCK = (T == 32) ? OMP_ZC32 : (MINB == 1 ? 4 : kZC);
-  constexpr int ZRK = (MINB == 1) ? 8 : 4;
-  constexpr int FZN = FSM ? 0 : (MINB == 1 ? 16 : 8);
+#ifndef OMP_FEW_ZR
+#define OMP_FEW_ZR 8
+#endif
+#ifndef OMP_FEW_FZN
+#define OMP_FEW_FZN 16
+#endif
+  constexpr int ZRK = (MINB == 1) ? OMP_FEW_ZR : 4;
+  constexpr int FZN = FSM ? 0 : (MINB == 1 ? OMP_FEW_FZN : 8);
 #ifdef OMP_UPDATE_TRACE
   append_residual<T, CH, P, ZCK, SEL == SEL_PROJ, FZN, FSM && (T <= OMP_ZLANE_TMAX), ZRK>(a, b, k, n, sel_c, sm, FSM ? Fs : a.F + b * a.ldf, nullptr, nullptr,
                                                         &upd_t0_);
