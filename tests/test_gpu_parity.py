@@ -246,15 +246,18 @@ def test_overflowing_screen_groups_find_the_exact_argmax(mode):
     Q1 = np.linalg.qr(rng.standard_normal((M, M)))[0]
     Q2 = np.linalg.qr(rng.standard_normal((M, M)))[0]
     A = np.concatenate([Q1, Q2], axis=1).astype(np.float32)          # N = 512: four 128-atom groups
-    Y = np.zeros((4, M), dtype=np.float32)
-    for b, start in enumerate((0, 3, 40, 100)):                      # 12 tied atoms inside group 0
+    # 12 tied atoms inside group 0; starts 58 and 62 straddle atom 64, where (K = 256 < 1536) the screen's
+    # 16-warp epilogue splits the group between two warps that merge their in-window lists
+    starts = (0, 3, 40, 100, 58, 62)
+    Y = np.zeros((len(starts), M), dtype=np.float32)
+    for b, start in enumerate(starts):
         Y[b] = A[:, start:start + 12].astype(np.float64).sum(axis=1).astype(np.float32)
     scr = run_gpu(A, Y, 12, None, mode)
     small = run_gpu(A, Y, 12, None, "small")
     assert scr["path"] == "residual" and small["path"] == "small"
     for key in ("support", "X", "resid", "n_iter", "status"):
         assert np.array_equal(scr[key], small[key]), key
-    for b, start in enumerate((0, 3, 40, 100)):                      # every tied atom is recovered
+    for b, start in enumerate(starts):                               # every tied atom is recovered
         assert set(scr["support"][b].tolist()) == set(range(start, start + 12))
 
 
@@ -637,3 +640,35 @@ def test_persisting_l2_limit_is_restored():
     h2.close()
     assert limit() == before
     assert raised > before
+
+
+_EPI_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+from gpu_helpers import run_gpu
+from synth import make_problem
+prob = make_problem(sys.argv[2], B=int(sys.argv[3]))
+out = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+np.savez(sys.argv[4], **{k: out[k] for k in ("support", "X", "resid", "n_iter", "status")})
+"""
+
+
+@pytest.mark.parametrize("name,B", [("c5", 300), ("c2", 257), ("c3", 200)])
+def test_screen_epilogue_warp_count_bitwise(name, B, tmp_path):
+    """Below K = 1536 the screen's epilogue runs on 16 warps (64 columns each, the two warps of a 128-atom
+    group merging their in-window lists), above on 8.  The partial lists, hence every result, must be
+    the same bits either way: compared against a process that forces the 8-warp epilogue
+    (OMP_B200_EPI16_KMAX=0)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prob = make_problem(name, B=B)
+    mine = run_gpu(prob.A, prob.Y, prob.S, prob.eps, "bf16")
+    f = tmp_path / "epi8.npz"
+    env = dict(os.environ, OMP_B200_EPI16_KMAX="0")
+    subprocess.run([sys.executable, "-c", _EPI_SCRIPT, root, name, str(B), str(f)], env=env, check=True,
+                   timeout=600)
+    other = np.load(f)
+    for key in ("support", "X", "resid", "n_iter", "status"):
+        assert np.array_equal(mine[key], other[key]), key
