@@ -492,7 +492,10 @@ static cudaError_t launch_r(const UpdateArgs& a, int64_t B, size_t smem, size_t 
                                   : launch_tc<SEL, 64, 1>(a, B, smem, persist, few, mid, st);
   if (q4 <= 128) return wide_batch ? launch_tc<SEL, 32, 4>(a, B, smem, persist, few, mid, st)
                                    : launch_tc<SEL, 128, 1>(a, B, smem, persist, few, mid, st);
-  if (q4 <= 256) return launch_tc<SEL, 128, 2>(a, B, smem, persist, few, mid, st);
+#ifndef OMP_Q256_T
+#define OMP_Q256_T 128
+#endif
+  if (q4 <= 256) return launch_tc<SEL, OMP_Q256_T, 256 / OMP_Q256_T>(a, B, smem, persist, few, mid, st);
   if (q4 <= 512) return launch_tc<SEL, 128, 4>(a, B, smem, persist, few, mid, st);
   if (q4 <= 1024) return launch_tc<SEL, 256, 4>(a, B, smem, persist, few, mid, st);
   if (q4 <= 2048) return launch_tc<SEL, 256, 8>(a, B, smem, persist, few, mid, st);
