@@ -188,7 +188,10 @@ __global__ void __launch_bounds__(T, MINB) k_update(const UpdateArgs a) {
   if constexpr (!FSM) {
     const char* fp = reinterpret_cast<const char*>(a.F + b * a.ldf);
     // (only while F_k fits L1 comfortably; a large one is read from L2 with loads in flight instead)
-    const uint32_t fbytes = (uint32_t)min((int64_t)k * (k + 1) / 2 * 4, (int64_t)64 * 1024);
+#ifndef OMP_FPF_MAX
+#define OMP_FPF_MAX (64 * 1024)
+#endif
+    const uint32_t fbytes = (uint32_t)min((int64_t)k * (k + 1) / 2 * 4, (int64_t)OMP_FPF_MAX);
     for (uint32_t o = (uint32_t)tid * 128u; o < fbytes; o += (uint32_t)T * 128u)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fp + o));
   }
